@@ -1,0 +1,544 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 multi-ring parameter average (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload bert|resnet50|gpt2] [--acc f64|native] [--lanes 1|R]
+
+Metric (BASELINE.json): param-averaging bus GB/s and ms/round.  A step is
+one averaging cycle over the whole parameter set of every cluster (all
+rings).  bus GB/s follows the NCCL convention per GPU,
+busbw = S/t * 2(C-1)/C with S the fp32 bytes of one cluster's parameters;
+``value`` is the whole-job aggregate, N_gpus * busbw.
+
+N = 1 : C = 8 clusters co-resident on cuda:0 (one kernel, HBM-bound).
+N > 1 : torchrun, one process per GPU, one cluster per GPU (C = N),
+        DistRingGroup: one kernel per rank, peer loads/stores over NVLink.
+
+``--impl reference`` times the CPU oracle port (oracle/ring_oracle.c, all
+host threads) on a bounded sample of the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# tensor-boundary ring lengths (torchvision / transformers shapes)
+WORKLOADS = {
+    "resnet50": [6308928, 6172672, 5511168, 7564264],
+    "bert": [26201088, 27168768, 27170304, 28942080],
+    "gpt2": [51463168, 43039744, 41987072, 41986048, 41989120, 41987072, 41986048, 50384896],
+}
+WORKLOAD_NAMES = {
+    "resnet50": "ResNet-50 parameter set (25,557,032 fp32), 4 rings",
+    "bert": "BERT-base parameter set (109,482,240 fp32), 4 submodel rings",
+    "gpt2": "GPT-2 medium parameter set (354,823,168 fp32), 8 rings",
+}
+METRIC = "param-averaging bus GB/s and ms/round at 1/2/4/8 B200 vs NVLink roofline"
+NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
+SEED = 20241018
+SIGMA = 0.02
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ring_starts(lens):
+    out, s = [], 0
+    for n in lens:
+        out.append(s)
+        s += n
+    return out
+
+
+def busbw(total_params: int, c: int, seconds: float) -> float:
+    return total_params * 4 / seconds * 2 * (c - 1) / c / 1e9
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port; only bench.py's cpu_baseline / --impl reference use it)
+
+
+class CpuSample:
+    """A bounded sample of the workload for the CPU oracle: the first `frac`
+    of every ring (same C, same ring structure), fp32 N(0, 0.02)."""
+
+    def __init__(self, lens, c: int, budget_params: int):
+        import numpy as np
+
+        total = sum(lens)
+        frac = min(1.0, budget_params / total)
+        self.lens = [max(1, int(n * frac)) for n in lens]
+        self.total = sum(self.lens)
+        self.c = c
+        rng = np.random.Generator(np.random.Philox(key=SEED))
+        self.xs = [rng.standard_normal(self.total, dtype=np.float32) * np.float32(SIGMA) for _ in range(c)]
+        self.outs = [np.empty_like(x) for x in self.xs]
+
+    def run(self, threads: int) -> float:
+        """One cycle of the C oracle (f32 in, f64 fold, f32 out -- the product
+        contract); returns seconds."""
+        from oracle import c_oracle
+
+        t0 = time.perf_counter()
+        c_oracle.ring_mean_into(c_oracle.MODE_F32_ACC64, ring_starts(self.lens), self.lens, self.xs, None,
+                                self.outs, threads=threads)
+        return time.perf_counter() - t0
+
+
+def cpu_oracle_time(lens, c: int, budget_params: int, threads: int, repeats: int = 1):
+    smp = CpuSample(lens, c, budget_params)
+    smp.run(threads)
+    return smp.total, [smp.run(threads) for _ in range(repeats)]
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, n_gpus: int, rank: int):
+    if rank != 0:
+        return
+    lens = WORKLOADS[args.workload]
+    c = args.clusters or (8 if n_gpus == 1 else n_gpus)
+    threads = host_threads()
+    budget = args.cpu_sample_params
+    smp = CpuSample(lens, c, budget)
+    s_total = smp.total
+    for _ in range(args.warmup):
+        smp.run(threads)
+    steps = [smp.run(threads) for _ in range(args.steps)]
+    t = statistics.median(steps)
+    bw = busbw(s_total, c, t)
+    value = bw * n_gpus
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3 * sum(lens) / s_total, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 fold)",
+        "data": "synthetic N(0,0.02) fp32, Philox seeded",
+        "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
+                   "parallelism": f"cpu threads {threads}"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"first {s_total} of {sum(lens)} params per cluster (every ring scaled), "
+                                   f"C={c}, oracle/ring_oracle.c f32-in f64-fold, {cpu_model()}"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU legs
+
+
+def synth(total: int, key: int, device):
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(SEED * 1000 + key)
+    return torch.randn(total, device=device, generator=g, dtype=torch.float32) * SIGMA
+
+
+def time_steps(fn, stream, steps: int):
+    """Per-step CUDA-event durations (ms) on `stream`."""
+    import torch
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        a.record(stream)
+        fn()
+        b.record(stream)
+    return evs
+
+
+def run_single(args):
+    """N = 1: C clusters co-resident on cuda:0."""
+    import torch
+
+    from paper_2401_01728_b200.plan import LocalRingGroup
+
+    lens = WORKLOADS[args.workload]
+    c = args.clusters or 8
+    total = sum(lens)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    xs = [synth(total, m, dev) for m in range(c)]
+    g = LocalRingGroup(ring_starts(lens), lens, total, [0] * c, torch.float32, acc=args.acc, lanes=args.lanes)
+    g.bind_tensors(xs)
+    stream = torch.cuda.current_stream()
+    lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
+
+    def step():
+        if lane_streams:
+            for s in lane_streams:
+                s.wait_stream(stream)
+            g.run({0: lane_streams})
+            for s in lane_streams:
+                stream.wait_stream(s)
+        else:
+            g.run({0: [stream]})
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    g.check()
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    evs = time_steps(step, stream, args.steps)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    g.check()
+    total_ms = t_start.elapsed_time(t_end)
+    per = [a.elapsed_time(b) for a, b in evs]
+    ms = total_ms / args.steps
+    kernel_ms = statistics.mean(per)
+
+    # e2e: host (pinned) buffers -> device -> average -> host, via the C ABI
+    hsrc = [x.cpu().pin_memory() for x in xs]
+    hdst = [torch.empty_like(h).pin_memory() for h in hsrc]
+    plan = g.plans[0]
+    e2e_streams = [torch.cuda.Stream() for _ in range(len(lens))]
+    plan_e2e = LocalRingGroup(ring_starts(lens), lens, total, [0] * c, torch.float32, acc=args.acc,
+                              lanes=len(lens))
+    plan_e2e.bind_tensors(xs)
+    pe = plan_e2e.plans[0]
+
+    def e2e_step():
+        pe.run_host([h.data_ptr() for h in hsrc], [h.data_ptr() for h in hdst], e2e_streams)
+        for s in e2e_streams:
+            stream.wait_stream(s)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_steps = max(3, min(args.steps, 10))
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    for s in e2e_streams:
+        s.wait_stream(stream)
+    a.record(stream)
+    for _ in range(e_steps):
+        for s in e2e_streams:
+            s.wait_stream(stream)
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    plan_e2e.check()
+    e2e_ms = a.elapsed_time(b) / e_steps
+    del plan
+
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_bytes = 2 * c * total * 4
+    achieved = hbm_bytes / (kernel_ms * 1e-3) / 1e9
+    bw = busbw(total, c, ms * 1e-3)
+
+    # CPU baseline: the oracle port on a bounded sample, all host threads
+    threads = host_threads()
+    s_total, ct = cpu_oracle_time(lens, c, args.cpu_sample_params, threads, repeats=3)
+    cpu_bw = busbw(s_total, c, min(ct))
+
+    line = {
+        "metric": METRIC, "value": round(bw, 3), "unit": "GB/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "ms_per_round": round(ms / (2 * (c - 1)), 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
+        "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
+        "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
+                   "placement": "co-resident on cuda:0", "lanes": args.lanes, "parallelism": "replicas only",
+                   "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "basis": f"2*C*S = {hbm_bytes} B per launch (read C, write C vectors)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+        "cpu_baseline": {"value": round(cpu_bw, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"first {s_total} of {total} params per cluster, C={c}, "
+                                   f"oracle/ring_oracle.c, best of 3, {cpu_model()}"},
+        "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3), 3), "unit": "GB/s",
+                "ms_per_step": round(e2e_ms, 3),
+                "h2d_bytes_per_step": c * total * 4, "d2h_bytes_per_step": c * total * 4,
+                "path": "rv_allreduce_mean_host (pinned host fp32, per-ring lanes)"},
+        "gpu_launches": args.steps * args.lanes,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_multi(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_01728_b200.dist import DistRingGroup
+
+    lens = WORKLOADS[args.workload]
+    total = sum(lens)
+    dev = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(dev)
+    x = synth(total, rank, dev)
+    grp = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes)
+    stream = torch.cuda.current_stream()
+    lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
+
+    def step():
+        if lane_streams:
+            for s in lane_streams:
+                s.wait_stream(stream)
+            grp.average(lane_streams)
+            for s in lane_streams:
+                stream.wait_stream(s)
+        else:
+            grp.average([stream])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    grp.check()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    evs = time_steps(step, stream, args.steps)
+    b.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop() if clocks else None
+    grp.check()
+    ms_local = a.elapsed_time(b) / args.steps
+    kern_local = statistics.mean(ea.elapsed_time(eb) for ea, eb in evs)
+    t = torch.tensor([ms_local, kern_local], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # gloo, outside the timed region
+    ms, kernel_ms = float(t[0]), float(t[1])
+
+    # e2e through the host-buffer C ABI: pinned host -> GPU -> average -> host
+    hsrc = x.cpu().pin_memory()
+    hdst = torch.empty_like(hsrc).pin_memory()
+    grp_e2e = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=len(lens))
+    e2e_streams = [torch.cuda.Stream() for _ in lens]
+
+    def e2e_step():
+        for s in e2e_streams:
+            s.wait_stream(stream)
+        grp_e2e.average_host(hsrc, hdst, e2e_streams)
+        for s in e2e_streams:
+            stream.wait_stream(s)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e_steps = max(3, min(args.steps, 10))
+    ea = torch.cuda.Event(enable_timing=True)
+    eb = torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    eb.record(stream)
+    torch.cuda.synchronize()
+    grp_e2e.check()
+    te = torch.tensor([ea.elapsed_time(eb) / e_steps], dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te[0])
+
+    nccl = None
+    if args.nccl:
+        nccl = nccl_compare(lens, x, world, min(args.steps, 20))
+
+    if rank == 0:
+        c = world
+        bw = busbw(total, c, ms * 1e-3)
+        alg_bytes = 2 * (c - 1) / c * total * 4
+        achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": round(bw * world, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "ms_per_round": round(ms / (2 * (c - 1)), 5),
+            "bus_gbps_per_gpu": round(bw, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
+            "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
+            "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
+                       "placement": "one cluster per GPU", "lanes": args.lanes,
+                       "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
+                       "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
+            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
+                         "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
+                         "basis": f"2(C-1)/C*S = {int(alg_bytes)} B per GPU per launch, each direction",
+                         "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)"},
+            "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3) * world, 3), "unit": "GB/s",
+                    "ms_per_step": round(e2e_ms, 3),
+                    "h2d_bytes_per_step": world * total * 4, "d2h_bytes_per_step": world * total * 4,
+                    "path": "rv_allreduce_mean_host (pinned host fp32, per-ring lanes)"},
+            "gpu_launches": args.steps * args.lanes * world,
+            "clocks": clk,
+        }
+        if nccl:
+            line["nccl_compare"] = nccl
+        print(json.dumps(line), flush=True)
+    grp_e2e.close()
+    grp.close()
+
+
+def nccl_compare(lens, x, world: int, steps: int):
+    """NCCL comparison path: ncclAllReduce(avg) per ring on its own buffer
+    slice (one communicator; rings issued back to back).  Not parity-exact."""
+    import torch
+    import torch.distributed as dist
+
+    y = x.clone()
+    starts = ring_starts(lens)
+    views = [y[s:s + n] for s, n in zip(starts, lens)]
+
+    def step():
+        for v in views:
+            dist.all_reduce(v, op=dist.ReduceOp.AVG)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    s = torch.cuda.current_stream()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(steps):
+        step()
+    b.record(s)
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"ms_per_step": round(ms, 4), "bus_gbps_per_gpu": round(busbw(sum(lens), world, ms * 1e-3), 3),
+            "algo": os.environ.get("NCCL_ALGO", "default")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert")
+    ap.add_argument("--acc", choices=["f64", "native"], default="f64")
+    ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")
+    ap.add_argument("--cpu-sample-params", type=int, default=8_000_000)
+    ap.add_argument("--nccl", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = max(world, 1) if world > 1 else args.gpus
+
+    if args.impl == "reference":
+        run_reference(args, n_gpus, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        try:
+            run_multi(args, rank, world, local_rank)
+        finally:
+            dist.destroy_process_group()
+        return
+    run_single(args)
+
+
+if __name__ == "__main__":
+    main()

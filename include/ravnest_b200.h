@@ -1,0 +1,133 @@
+/*
+ * ravnest_b200 -- C ABI of the B200-native Parallel Multi-Ring All-Reduce.
+ *
+ * Drop-in for the averaging path of Ravnest (arXiv 2401.01728); reference
+ * paths below are /root/reference/pkg/src/ravnest/<file>:<line>.
+ *
+ * Model.  C clusters ("members" of every ring, ascending cluster id =
+ * position 0..C-1) each hold a flat parameter vector of total_params
+ * elements.  The schedule cuts [0, total_params) into R rings
+ * (RingSchedule, multiring.py:31-53, built by build_ring_schedule
+ * :56-105).  One cycle leaves every member holding, for chunk k of every ring
+ * (chunk_bounds, multiring.py:134-144),
+ *
+ *     fl( fl(...fl(x_k + x_{k+1}) ... + x_{k+C-1}) / C )      (indices mod C)
+ *
+ * -- bit for bit what apply_ring_mean (multiring.py:302-333) and
+ * AllReduceController (multiring.py:154-247) compute.
+ *
+ * Execution.  A plan lives on ONE device and folds the chunks of the
+ * positions hosted there ("local" positions).  Each chunk k is read from all
+ * C member buffers (local HBM or peer memory over NVLink), folded in ring
+ * order, divided by C, and written to all C member buffers -- reduce-scatter
+ * and all-gather in one kernel.  Devices synchronise through release/acquire
+ * flags in each other's memory (no host round trip).  With every position on
+ * one device (n_ranks == 1) no flags are used.
+ *
+ * All calls return an int status (RV_OK or RV_E_*); rv_last_error() gives a
+ * thread-local message.  Calls on one plan are not re-entrant.
+ */
+#ifndef RAVNEST_B200_H
+#define RAVNEST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RV_ABI_VERSION 1
+#define RV_MAX_CLUSTERS 16
+#define RV_MAX_RANKS 16
+
+/* Status codes; the Python shim maps them onto the reference's exception
+ * hierarchy (errors.py:4-65). */
+#define RV_OK 0
+#define RV_E_CONFIG 1      /* ConfigError: C < 2, dtype/mode (multiring.py:268-269)          */
+#define RV_E_LAYOUT 2      /* LayoutError: rings do not tile [0,total) (multiring.py:108-116) */
+#define RV_E_CUDA 3        /* RavnestError: CUDA runtime failure                              */
+#define RV_E_PEER_ACCESS 4 /* RavnestError: peer / IPC mapping unavailable                    */
+#define RV_E_TIMEOUT 5     /* StallError: a peer never arrived (multiring.py:296-298)         */
+#define RV_E_ARG 6         /* RavnestError: null / unbound / misaligned argument              */
+
+#define RV_DTYPE_F32 0
+#define RV_DTYPE_F64 1
+
+/* Accumulation: RV_ACC_F64 folds in float64 and rounds once to the storage
+ * dtype -- the reference works in float64 (multiring.py:276,309), so fp32
+ * outputs equal float32(reference) bit for bit.  RV_ACC_NATIVE folds in the
+ * storage dtype (the fp32 ring order).  For RV_DTYPE_F64 both are the same. */
+#define RV_ACC_F64 0
+#define RV_ACC_NATIVE 1
+
+typedef struct rv_plan rv_plan;
+
+int rv_version(void);
+const char *rv_last_error(void);
+const char *rv_status_string(int status);
+
+/* Replaces: consuming RingSchedule (multiring.py:31-53) + the validation of
+ * run_allreduce (:267-275) and validate_schedule's tiling check (:108-116).
+ * Rings must tile [0, total_params) in order; zero-length rings are legal. */
+int rv_plan_create(rv_plan **out, int device, int n_clusters, int n_rings,
+                   const int64_t *ring_start, const int64_t *ring_len,
+                   int64_t total_params, int dtype, int acc_mode);
+
+/* Member buffers as seen from the plan's device (local, peer-mapped or
+ * IPC-imported).  src is read, dst is written; dst == src is in place.
+ * Replaces the per-cluster working arrays (multiring.py:276,309). */
+int rv_plan_bind(rv_plan *plan, int pos, const void *src, void *dst);
+
+/* Positions hosted by this device: their chunks are folded here. */
+int rv_plan_set_local(rv_plan *plan, const int *positions, int n_positions);
+
+/* 1 = one launch covers all rings; n_rings = one launch per ring (ring r on
+ * stream r % n_streams), the north-star "one stream per ring". */
+int rv_plan_set_lanes(rv_plan *plan, int n_lanes);
+
+/* This plan's flag area (device memory, cudaMalloc'd: IPC-exportable). */
+int rv_plan_flag_area(rv_plan *plan, void **flags, size_t *bytes);
+
+/* Multi-device group: this plan is `rank` of `n_ranks`; peer_flag_areas[r] is
+ * rank r's flag area mapped into this device (entry `rank` is ignored). */
+int rv_plan_set_peers(rv_plan *plan, int rank, int n_ranks, void *const *peer_flag_areas);
+
+int rv_plan_set_timeout(rv_plan *plan, double seconds);
+
+/* One averaging cycle, asynchronous on the given CUDA streams (NULL/0 ->
+ * the legacy default stream).  Replaces apply_ring_mean / run_allreduce /
+ * AllReduceController.kickoff..done (multiring.py:180-232, 254-333). */
+int rv_allreduce_mean(rv_plan *plan, void *const *streams, int n_streams);
+
+/* Same cycle with HOST buffers for the local positions: per lane, copy the
+ * lane's ring ranges host->device, average, copy device->host, pipelined
+ * across lanes.  host_src/host_dst are indexed like rv_plan_set_local's
+ * positions (pinned memory for overlap). */
+int rv_allreduce_mean_host(rv_plan *plan, const void *const *host_src, void *const *host_dst,
+                           void *const *streams, int n_streams);
+
+/* Blocking: device-side status of the plan (RV_OK or RV_E_TIMEOUT), and a
+ * description of the first stall "(ring=r, phase=..., member=m)". */
+int rv_plan_status(rv_plan *plan, char *diag, size_t diag_len);
+int rv_plan_reset_status(rv_plan *plan);
+int rv_plan_destroy(rv_plan *plan);
+
+/* Delayed-update blend: live <- mean + (live - snap),
+ * and exactly mean where live == snap bitwise. */
+int rv_blend(int device, int dtype, void *live, const void *snap, const void *mean,
+             int64_t n, void *stream);
+
+/* Memory plumbing for multi-process groups (one process per GPU). */
+int rv_ipc_handle_size(void);
+int rv_ipc_export(const void *dev_ptr, void *handle_out, uint64_t *offset_out);
+int rv_ipc_import(int device, const void *handle, uint64_t offset, void **dev_ptr_out);
+int rv_ipc_close(int device, void *dev_ptr);
+int rv_enable_peer_access(int device, int peer);
+int rv_device_sm_count(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAVNEST_B200_H */

@@ -1,0 +1,930 @@
+// ravnest_b200 -- sm_100a kernels and C ABI for the Parallel Multi-Ring
+// All-Reduce of Ravnest (arXiv 2401.01728).  See include/ravnest_b200.h for
+// the contract and DESIGN.md for the data layout and roofline.
+//
+// Reference arithmetic (/root/reference/pkg/src/ravnest/multiring.py):
+//   * chunk split       :134-144  chunk i of a ring gets base + (i < rem)
+//   * reduce-scatter    :216-219  seg += payload, last RS round seg /= C
+//   * all-gather        :220-221  seg = payload
+// Closed form (SURVEY.md headline fact 3): chunk k of every member ends as
+//   fl(fl(...fl(x_k + x_{k+1}) ... + x_{k+C-1}) / C), indices mod C.
+//
+// One kernel does the whole cycle for the chunks hosted on this device: it
+// reads chunk k from the C member buffers (local HBM or NVLink peer memory),
+// folds in ring order, divides by C and stores the mean into all C member
+// buffers.  Chunk k is read and written only by its owner, so in-place
+// averaging needs no mid-cycle barrier; cross-device ordering uses
+// release/acquire flags at system scope (arrive before the first read,
+// depart after the last write).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ravnest_b200.h"
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// error plumbing
+
+thread_local std::string g_err;
+
+int set_err(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define RV_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return set_err(RV_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));   \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// device-side types
+
+constexpr int kThreads = 256;
+constexpr unsigned kStatusTimeout = 1u;
+
+struct Seg {
+  int64_t lo, hi;            // chunk [lo, hi) in elements
+  int64_t body_lo, body_hi;  // 16-byte aligned vector body inside it
+  int32_t k;                 // fold start position (chunk index in its ring)
+  int32_t ring;
+};
+
+struct LaneState {
+  unsigned long long epoch;     // cycles completed on this lane
+  unsigned long long signaled;  // last epoch whose arrive flags were posted
+  unsigned int done;            // blocks finished in the running cycle
+  unsigned int pad;
+};
+
+struct CycleParams {
+  const void *src[RV_MAX_CLUSTERS];
+  void *dst[RV_MAX_CLUSTERS];
+  unsigned long long *peer_flags[RV_MAX_RANKS];  // rank r's flag area (as mapped here)
+  const Seg *segs;
+  const int64_t *tile_prefix;  // nseg + 1 entries
+  unsigned long long *my_flags;
+  LaneState *state;
+  unsigned int *status;  // [0] code, [1] diag
+  int64_t n_tiles;
+  unsigned long long timeout_ns;
+  double inv_c;
+  int C, nseg, rank, n_ranks, lane, pow2;
+};
+
+// flag slot of (lane, sender rank, phase) inside a receiver's flag area
+__host__ __device__ inline size_t flag_index(int lane, int sender, int phase) {
+  return ((size_t)lane * RV_MAX_RANKS + (size_t)sender) * 2 + (size_t)phase;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Wait until every peer posted `phase` for epoch e.  Returns false on timeout.
+__device__ bool wait_peers(const CycleParams &p, int phase, unsigned long long e) {
+  const unsigned long long t0 = globaltimer();
+  for (int r = 0; r < p.n_ranks; ++r) {
+    if (r == p.rank) continue;
+    const unsigned long long *f = p.my_flags + flag_index(p.lane, r, phase);
+    unsigned spins = 0;
+    while (ld_acquire_sys(f) < e) {
+      if ((++spins & 255u) == 0) {
+        if (*(volatile unsigned *)p.status != 0) return false;
+        if (globaltimer() - t0 > p.timeout_ns) {
+          if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u)
+            p.status[1] = ((unsigned)phase << 16) | ((unsigned)p.lane << 8) | (unsigned)r;
+          return false;
+        }
+      }
+    }
+  }
+  return true;
+}
+
+__device__ void post_peers(const CycleParams &p, int phase, unsigned long long e) {
+  for (int r = 0; r < p.n_ranks; ++r) {
+    if (r == p.rank) continue;
+    st_release_sys(p.peer_flags[r] + flag_index(p.lane, p.rank, phase), e);
+  }
+}
+
+template <int VB>
+struct RawVec;
+template <>
+struct RawVec<16> {
+  using type = uint4;
+};
+template <>
+struct RawVec<8> {
+  using type = uint2;
+};
+template <>
+struct RawVec<4> {
+  using type = unsigned int;
+};
+
+template <typename T, int VB>
+union Lanes {
+  typename RawVec<VB>::type raw;
+  T v[VB / sizeof(T)];
+};
+
+template <typename T, typename Acc>
+__device__ __forceinline__ T finish(Acc acc, const CycleParams &p) {
+  // IEEE true division by C (multiring.py:219).  For C a power of two the
+  // product with the exact reciprocal is the same correctly rounded value.
+  const Acc q = p.pow2 ? acc * (Acc)p.inv_c : acc / (Acc)p.C;
+  return (T)q;
+}
+
+// Scalar fold of element i (chunk edges and misaligned buffers).
+template <typename T, typename Acc>
+__device__ __forceinline__ void fold_scalar(const CycleParams &p, int k, int64_t i) {
+  int m = k;
+  Acc acc = (Acc)__ldcs(static_cast<const T *>(p.src[m]) + i);
+  for (int q = 1; q < p.C; ++q) {
+    m = (m + 1 == p.C) ? 0 : m + 1;
+    acc = acc + (Acc)__ldcs(static_cast<const T *>(p.src[m]) + i);
+  }
+  const T out = finish<T, Acc>(acc, p);
+  for (int q = 0; q < p.C; ++q) __stcs(static_cast<T *>(p.dst[q]) + i, out);
+}
+
+// CB: compile-time capacity for C (2/4/8/16), VB: vector bytes, U: vectors
+// per thread per tile.  U*CB independent loads are in flight per thread.
+template <typename T, typename Acc, int CB, int VB, int U>
+__global__ void __launch_bounds__(kThreads)
+ring_cycle_kernel(const __grid_constant__ CycleParams p) {
+  constexpr int N = VB / sizeof(T);
+  using Raw = typename RawVec<VB>::type;
+  __shared__ int s_go;
+  unsigned long long epoch = 0;
+
+  if (p.n_ranks > 1) {
+    if (threadIdx.x == 0) {
+      epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
+      int go = (*(volatile unsigned *)p.status == 0);
+      if (go) {
+        // first block of this launch posts "inputs final" to every peer
+        if (atomicCAS(&p.state->signaled, epoch - 1ull, epoch) == epoch - 1ull) {
+          __threadfence_system();
+          post_peers(p, 0, epoch);
+        }
+        go = wait_peers(p, 0, epoch);
+      }
+      s_go = go;
+    }
+    __syncthreads();
+  } else {
+    if (threadIdx.x == 0) s_go = 1;
+    __syncthreads();
+  }
+
+  if (s_go) {
+    const int64_t tile_vecs = (int64_t)kThreads * U;
+    for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+      int a = 0, b = p.nseg - 1;
+      while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
+      }
+      const Seg s = p.segs[a];
+      const int64_t local_tile = t - __ldg(p.tile_prefix + a);
+      const int64_t nvec = (s.body_hi - s.body_lo) / N;
+      const int64_t j0 = local_tile * tile_vecs + threadIdx.x;
+
+      Lanes<T, VB> x[U][CB];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + (int64_t)u * kThreads;
+        if (j < nvec) {
+          const int64_t off = s.body_lo + j * N;
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            if (q < p.C) {
+              int m = s.k + q;
+              if (m >= p.C) m -= p.C;
+              x[u][q].raw = __ldcs(reinterpret_cast<const Raw *>(static_cast<const T *>(p.src[m]) + off));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = j0 + (int64_t)u * kThreads;
+        if (j < nvec) {
+          Lanes<T, VB> out;
+#pragma unroll
+          for (int e = 0; e < N; ++e) {
+            Acc acc = (Acc)x[u][0].v[e];
+#pragma unroll
+            for (int q = 1; q < CB; ++q)
+              if (q < p.C) acc = acc + (Acc)x[u][q].v[e];
+            out.v[e] = finish<T, Acc>(acc, p);
+          }
+          const int64_t off = s.body_lo + j * N;
+#pragma unroll
+          for (int q = 0; q < CB; ++q)
+            if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + off), out.raw);
+        }
+      }
+      if (local_tile == 0) {
+        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+        if ((int64_t)threadIdx.x < nhead + ntail) {
+          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
+                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
+          fold_scalar<T, Acc>(p, s.k, i);
+        }
+      }
+    }
+  }
+
+  if (p.n_ranks > 1) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();  // this block's peer stores before the count
+      const unsigned prev = atomicAdd(&p.state->done, 1u);
+      if (prev == gridDim.x - 1) {
+        __threadfence_system();  // every block's stores are ordered before the post
+        post_peers(p, 1, epoch);
+        if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
+        p.state->done = 0u;
+        *(volatile unsigned long long *)&p.state->epoch = epoch;
+        __threadfence();
+      }
+    }
+  }
+}
+
+// live <- mean + (live - snap); exactly mean where live == snap bitwise.
+template <typename T, typename U>
+__global__ void __launch_bounds__(kThreads)
+blend_kernel(T *__restrict__ live, const T *__restrict__ snap, const T *__restrict__ mean, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T l = live[i], s = snap[i], m = __ldcs(mean + i);
+    U lb, sb;
+    memcpy(&lb, &l, sizeof(T));
+    memcpy(&sb, &s, sizeof(T));
+    live[i] = (lb == sb) ? m : (m + (l - s));
+  }
+}
+
+template <typename T, typename U>
+__global__ void __launch_bounds__(kThreads)
+blend_kernel_v4(T *__restrict__ live, const T *__restrict__ snap, const T *__restrict__ mean, int64_t nvec) {
+  constexpr int N = 16 / sizeof(T);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nvec; j += stride) {
+    Lanes<T, 16> l, s, m, o;
+    l.raw = *reinterpret_cast<const uint4 *>(live + j * N);
+    s.raw = __ldcs(reinterpret_cast<const uint4 *>(snap + j * N));
+    m.raw = __ldcs(reinterpret_cast<const uint4 *>(mean + j * N));
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      U lb, sb;
+      memcpy(&lb, &l.v[e], sizeof(T));
+      memcpy(&sb, &s.v[e], sizeof(T));
+      o.v[e] = (lb == sb) ? m.v[e] : (m.v[e] + (l.v[e] - s.v[e]));
+    }
+    *reinterpret_cast<uint4 *>(live + j * N) = o.raw;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+
+using KernelFn = void (*)(CycleParams);
+
+enum Mode { kF32Acc64 = 0, kF32Native = 1, kF64 = 2 };
+
+template <typename T, typename Acc, int VB>
+KernelFn pick_cb(int c) {
+  if (c <= 2) return ring_cycle_kernel<T, Acc, 2, VB, 8>;
+  if (c <= 4) return ring_cycle_kernel<T, Acc, 4, VB, 4>;
+  if (c <= 8) return ring_cycle_kernel<T, Acc, 8, VB, 2>;
+  return ring_cycle_kernel<T, Acc, 16, VB, 1>;
+}
+
+KernelFn pick_kernel(int mode, int c, bool vec, int *u_out) {
+  *u_out = c <= 2 ? 8 : c <= 4 ? 4 : c <= 8 ? 2 : 1;
+  switch (mode) {
+    case kF32Acc64: return vec ? pick_cb<float, double, 16>(c) : pick_cb<float, double, 4>(c);
+    case kF32Native: return vec ? pick_cb<float, float, 16>(c) : pick_cb<float, float, 4>(c);
+    default: return vec ? pick_cb<double, double, 16>(c) : pick_cb<double, double, 8>(c);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// driver entry point for cuMemGetAddressRange (no link-time libcuda dependency)
+
+typedef int (*PFN_getAddressRange)(unsigned long long *, size_t *, unsigned long long);
+
+int alloc_base(const void *ptr, unsigned long long *base) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !f) return set_err(RV_E_CUDA, "cuMemGetAddressRange unavailable");
+    fn = reinterpret_cast<PFN_getAddressRange>(f);
+  }
+  size_t size = 0;
+  int rc = fn(base, &size, (unsigned long long)(uintptr_t)ptr);
+  if (rc != 0) return set_err(RV_E_ARG, "cuMemGetAddressRange(%p) failed (%d)", ptr, rc);
+  return RV_OK;
+}
+
+struct IpcEntry {
+  void *base;
+  int refs;
+};
+std::mutex g_ipc_mu;
+std::map<std::pair<int, std::string>, IpcEntry> g_ipc;  // (device, handle bytes) -> mapping
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// plan
+
+struct rv_plan {
+  int device = 0;
+  int C = 0, R = 0;
+  int64_t total = 0;
+  int dtype = RV_DTYPE_F32, acc = RV_ACC_F64;
+  std::vector<int64_t> rstart, rlen;
+  std::vector<const void *> src;
+  std::vector<void *> dst;
+  std::vector<char> bound;
+  std::vector<int> local;
+  int n_lanes = 1;
+  int rank = 0, n_ranks = 1;
+  std::vector<unsigned long long *> peer_flags;
+  unsigned long long *flags = nullptr;  // capacity max(R,1) lanes x RV_MAX_RANKS x 2
+  size_t flag_bytes = 0;
+  LaneState *states = nullptr;  // max(R,1)
+  unsigned int *status = nullptr;
+  unsigned long long timeout_ns = 20ull * 1000000000ull;
+  int sm_count = 0;
+  // built lane tables
+  bool dirty = true;       // local positions / lanes / peers changed
+  bool ptrs_dirty = true;  // buffers rebound: rebuild only if the alignment class changed
+  int built_vec = -1;
+  int64_t built_a0 = -1;
+  struct Lane {
+    Seg *segs = nullptr;
+    int64_t *prefix = nullptr;
+    int nseg = 0;
+    int64_t n_tiles = 0;
+    int64_t elems = 0;
+    std::vector<int> rings;
+    int grid = 0;
+  };
+  std::vector<Lane> lanes;
+  KernelFn kernel = nullptr;
+  int occ = 0;
+};
+
+namespace {
+
+void free_lanes(rv_plan *p) {
+  for (auto &l : p->lanes) {
+    if (l.segs) cudaFree(l.segs);
+    if (l.prefix) cudaFree(l.prefix);
+  }
+  p->lanes.clear();
+}
+
+int elem_size(int dtype) { return dtype == RV_DTYPE_F64 ? 8 : 4; }
+
+int build_tables(rv_plan *p) {
+  for (int i = 0; i < p->C; ++i)
+    if (!p->bound[i]) return set_err(RV_E_ARG, "cluster position %d is not bound", i);
+  if (p->local.empty()) return set_err(RV_E_ARG, "no local positions set");
+  const int es = elem_size(p->dtype);
+  // vector path needs every member buffer congruent modulo 16 bytes
+  const uintptr_t a = (uintptr_t)p->src[0] % 16;
+  bool vec = true;
+  for (int i = 0; i < p->C; ++i) {
+    if ((uintptr_t)p->src[i] % es || (uintptr_t)p->dst[i] % es)
+      return set_err(RV_E_ARG, "buffer of position %d is not %d-byte aligned", i, es);
+    if ((uintptr_t)p->src[i] % 16 != a || (uintptr_t)p->dst[i] % 16 != a) vec = false;
+  }
+  const int N = vec ? 16 / es : 1;
+  const int64_t a0 = vec ? (int64_t)(a / es) : 0;  // element i is vector aligned iff (i + a0) % N == 0
+  p->ptrs_dirty = false;
+  if (!p->dirty && p->built_vec == (int)vec && p->built_a0 == a0) return RV_OK;
+  p->built_vec = (int)vec;
+  p->built_a0 = a0;
+  const int mode = p->dtype == RV_DTYPE_F64 ? kF64 : (p->acc == RV_ACC_NATIVE ? kF32Native : kF32Acc64);
+  int U = 1;
+  p->kernel = pick_kernel(mode, p->C, vec, &U);
+  DeviceGuard g(p->device);
+  RV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ, p->kernel, kThreads, 0));
+  if (p->occ < 1) p->occ = 1;
+  const int64_t tile_vecs = (int64_t)kThreads * U;
+
+  free_lanes(p);
+  p->lanes.resize(p->n_lanes);
+  std::vector<int> loc = p->local;
+  std::sort(loc.begin(), loc.end());
+  int64_t all_elems = 0;
+  for (int l = 0; l < p->n_lanes; ++l) {
+    rv_plan::Lane &lane = p->lanes[l];
+    std::vector<Seg> segs;
+    std::vector<int64_t> prefix(1, 0);
+    for (int r = l; r < p->R; r += p->n_lanes) {
+      lane.rings.push_back(r);
+      const int64_t base = p->rlen[r] / p->C, rem = p->rlen[r] % p->C;
+      int64_t lo = p->rstart[r];
+      std::vector<std::pair<int64_t, int64_t>> bounds(p->C);
+      for (int k = 0; k < p->C; ++k) {  // multiring.py:134-144
+        const int64_t n = base + (k < rem ? 1 : 0);
+        bounds[k] = {lo, lo + n};
+        lo += n;
+      }
+      for (int k : loc) {
+        Seg s;
+        s.lo = bounds[k].first;
+        s.hi = bounds[k].second;
+        s.k = k;
+        s.ring = r;
+        if (s.hi <= s.lo) continue;
+        int64_t blo = s.lo + ((N - (s.lo + a0) % N) % N);
+        int64_t bhi = s.hi - ((s.hi + a0) % N);
+        if (bhi <= blo) {
+          blo = bhi = s.hi;  // no aligned vector: all edge elements (< 2N)
+        }
+        s.body_lo = blo;
+        s.body_hi = bhi;
+        const int64_t nvec = (bhi - blo) / N;
+        const int64_t tiles = std::max<int64_t>(1, (nvec + tile_vecs - 1) / tile_vecs);
+        segs.push_back(s);
+        prefix.push_back(prefix.back() + tiles);
+        lane.elems += s.hi - s.lo;
+      }
+    }
+    lane.nseg = (int)segs.size();
+    lane.n_tiles = prefix.back();
+    all_elems += lane.elems;
+    if (lane.nseg > 0) {
+      RV_CUDA(cudaMalloc(&lane.segs, sizeof(Seg) * segs.size()));
+      RV_CUDA(cudaMalloc(&lane.prefix, sizeof(int64_t) * prefix.size()));
+      RV_CUDA(cudaMemcpy(lane.segs, segs.data(), sizeof(Seg) * segs.size(), cudaMemcpyHostToDevice));
+      RV_CUDA(cudaMemcpy(lane.prefix, prefix.data(), sizeof(int64_t) * prefix.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  // persistent grid: all lanes together fit in one wave (no lane can starve
+  // another on this device while both wait on peers)
+  const int64_t capacity = (int64_t)p->sm_count * p->occ;
+  int64_t used = 0;
+  for (int l = 0; l < p->n_lanes; ++l) {
+    rv_plan::Lane &lane = p->lanes[l];
+    int64_t share = all_elems > 0 ? capacity * lane.elems / all_elems : 0;
+    if (p->n_lanes == 1) share = capacity;
+    share = std::max<int64_t>(1, std::min<int64_t>(share, std::max<int64_t>(1, lane.n_tiles)));
+    lane.grid = (int)share;
+    used += share;
+  }
+  (void)used;
+  p->dirty = false;
+  return RV_OK;
+}
+
+int launch_lane(rv_plan *p, int l, cudaStream_t st) {
+  rv_plan::Lane &lane = p->lanes[l];
+  CycleParams cp;
+  memset(&cp, 0, sizeof(cp));
+  for (int i = 0; i < p->C; ++i) {
+    cp.src[i] = p->src[i];
+    cp.dst[i] = p->dst[i];
+  }
+  for (int r = 0; r < p->n_ranks && r < RV_MAX_RANKS; ++r) cp.peer_flags[r] = p->peer_flags[r];
+  cp.segs = lane.segs;
+  cp.tile_prefix = lane.prefix;
+  cp.my_flags = p->flags;
+  cp.state = p->states + l;
+  cp.status = p->status;
+  cp.n_tiles = lane.n_tiles;
+  cp.timeout_ns = p->timeout_ns;
+  cp.C = p->C;
+  cp.nseg = lane.nseg;
+  cp.rank = p->rank;
+  cp.n_ranks = p->n_ranks;
+  cp.lane = l;
+  cp.pow2 = (p->C & (p->C - 1)) == 0;
+  cp.inv_c = 1.0 / (double)p->C;
+  if (lane.nseg == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet
+  int grid = std::max(1, lane.grid);
+  p->kernel<<<grid, kThreads, 0, st>>>(cp);
+  RV_CUDA(cudaGetLastError());
+  return RV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rv_version(void) { return RV_ABI_VERSION; }
+
+const char *rv_last_error(void) { return g_err.c_str(); }
+
+const char *rv_status_string(int status) {
+  switch (status) {
+    case RV_OK: return "ok";
+    case RV_E_CONFIG: return "config error";
+    case RV_E_LAYOUT: return "layout error";
+    case RV_E_CUDA: return "CUDA error";
+    case RV_E_PEER_ACCESS: return "peer access unavailable";
+    case RV_E_TIMEOUT: return "peer stall (timeout)";
+    case RV_E_ARG: return "invalid argument";
+    default: return "unknown status";
+  }
+}
+
+int rv_plan_create(rv_plan **out, int device, int n_clusters, int n_rings, const int64_t *ring_start,
+                   const int64_t *ring_len, int64_t total_params, int dtype, int acc_mode) {
+  if (!out) return set_err(RV_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (n_clusters < 2)  // multiring.py:268-269
+    return set_err(RV_E_CONFIG, "all-reduce needs at least 2 clusters (got %d)", n_clusters);
+  if (n_clusters > RV_MAX_CLUSTERS)
+    return set_err(RV_E_CONFIG, "at most %d clusters supported (got %d)", RV_MAX_CLUSTERS, n_clusters);
+  if (dtype != RV_DTYPE_F32 && dtype != RV_DTYPE_F64) return set_err(RV_E_CONFIG, "unknown dtype %d", dtype);
+  if (acc_mode != RV_ACC_F64 && acc_mode != RV_ACC_NATIVE)
+    return set_err(RV_E_CONFIG, "unknown accumulation mode %d", acc_mode);
+  if (n_rings < 0 || total_params < 0 || (n_rings > 0 && (!ring_start || !ring_len)))
+    return set_err(RV_E_ARG, "bad ring arrays");
+  int64_t cursor = 0;  // multiring.py:110-116
+  for (int r = 0; r < n_rings; ++r) {
+    if (ring_start[r] != cursor || ring_len[r] < 0)
+      return set_err(RV_E_LAYOUT, "rings do not tile the parameter space (ring %d)", r);
+    cursor += ring_len[r];
+  }
+  if (cursor != total_params) return set_err(RV_E_LAYOUT, "rings do not cover all parameters");
+  int ndev = 0;
+  RV_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return set_err(RV_E_ARG, "device %d out of range (%d devices)", device, ndev);
+
+  rv_plan *p = new rv_plan();
+  p->device = device;
+  p->C = n_clusters;
+  p->R = n_rings;
+  p->total = total_params;
+  p->dtype = dtype;
+  p->acc = dtype == RV_DTYPE_F64 ? RV_ACC_F64 : acc_mode;
+  p->rstart.assign(ring_start, ring_start + n_rings);
+  p->rlen.assign(ring_len, ring_len + n_rings);
+  p->src.assign(n_clusters, nullptr);
+  p->dst.assign(n_clusters, nullptr);
+  p->bound.assign(n_clusters, 0);
+  p->peer_flags.assign(RV_MAX_RANKS, nullptr);
+  if (const char *t = getenv("RAVNEST_B200_TIMEOUT_S")) {
+    const double s = atof(t);
+    if (s > 0) p->timeout_ns = (unsigned long long)(s * 1e9);
+  }
+  {
+    DeviceGuard g(device);
+    cudaError_t e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device);
+    const int lanes_cap = std::max(1, n_rings);
+    p->flag_bytes = sizeof(unsigned long long) * flag_index(lanes_cap, 0, 0);
+    if (e == cudaSuccess) e = cudaMalloc(&p->flags, p->flag_bytes);
+    if (e == cudaSuccess) e = cudaMemset(p->flags, 0, p->flag_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->states, sizeof(LaneState) * lanes_cap);
+    if (e == cudaSuccess) e = cudaMemset(p->states, 0, sizeof(LaneState) * lanes_cap);
+    if (e == cudaSuccess) e = cudaMalloc(&p->status, 4 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(p->status, 0, 4 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      rv_plan_destroy(p);
+      return set_err(RV_E_CUDA, "plan allocation failed: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = p;
+  return RV_OK;
+}
+
+int rv_plan_bind(rv_plan *p, int pos, const void *src, void *dst) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  if (pos < 0 || pos >= p->C) return set_err(RV_E_ARG, "position %d out of range", pos);
+  if (!src || !dst) return set_err(RV_E_ARG, "NULL buffer for position %d", pos);
+  p->src[pos] = src;
+  p->dst[pos] = dst;
+  p->bound[pos] = 1;
+  p->ptrs_dirty = true;
+  return RV_OK;
+}
+
+int rv_plan_set_local(rv_plan *p, const int *positions, int n) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  if (n < 0 || (n > 0 && !positions)) return set_err(RV_E_ARG, "bad positions");
+  std::vector<char> seen(p->C, 0);
+  for (int i = 0; i < n; ++i) {
+    if (positions[i] < 0 || positions[i] >= p->C || seen[positions[i]])
+      return set_err(RV_E_ARG, "bad or repeated position %d", positions[i]);
+    seen[positions[i]] = 1;
+  }
+  p->local.assign(positions, positions + n);
+  p->dirty = true;
+  return RV_OK;
+}
+
+int rv_plan_set_lanes(rv_plan *p, int n_lanes) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  if (n_lanes < 1 || n_lanes > std::max(1, p->R))
+    return set_err(RV_E_ARG, "lanes must be in [1, %d]", std::max(1, p->R));
+  p->n_lanes = n_lanes;
+  p->dirty = true;
+  return RV_OK;
+}
+
+int rv_plan_flag_area(rv_plan *p, void **flags, size_t *bytes) {
+  if (!p || !flags) return set_err(RV_E_ARG, "NULL argument");
+  *flags = p->flags;
+  if (bytes) *bytes = p->flag_bytes;
+  return RV_OK;
+}
+
+int rv_plan_set_peers(rv_plan *p, int rank, int n_ranks, void *const *areas) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  if (n_ranks < 1 || n_ranks > RV_MAX_RANKS || rank < 0 || rank >= n_ranks)
+    return set_err(RV_E_ARG, "bad rank %d of %d", rank, n_ranks);
+  if (n_ranks > 1 && !areas) return set_err(RV_E_ARG, "peer flag areas missing");
+  p->rank = rank;
+  p->n_ranks = n_ranks;
+  for (int r = 0; r < RV_MAX_RANKS; ++r)
+    p->peer_flags[r] = (r < n_ranks && areas) ? static_cast<unsigned long long *>(areas[r]) : nullptr;
+  for (int r = 0; r < n_ranks; ++r)
+    if (r != rank && !p->peer_flags[r]) return set_err(RV_E_ARG, "flag area of rank %d missing", r);
+  p->dirty = true;
+  return RV_OK;
+}
+
+int rv_plan_set_timeout(rv_plan *p, double seconds) {
+  if (!p || !(seconds > 0)) return set_err(RV_E_ARG, "bad timeout");
+  p->timeout_ns = (unsigned long long)(seconds * 1e9);
+  return RV_OK;
+}
+
+int rv_allreduce_mean(rv_plan *p, void *const *streams, int n_streams) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  DeviceGuard g(p->device);
+  if (p->dirty || p->ptrs_dirty) {
+    int rc = build_tables(p);
+    if (rc) return rc;
+  }
+  for (int l = 0; l < p->n_lanes; ++l) {
+    cudaStream_t st = (streams && n_streams > 0) ? (cudaStream_t)streams[l % n_streams] : (cudaStream_t)0;
+    int rc = launch_lane(p, l, st);
+    if (rc) return rc;
+  }
+  return RV_OK;
+}
+
+int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const *host_dst,
+                           void *const *streams, int n_streams) {
+  if (!p || !host_src || !host_dst) return set_err(RV_E_ARG, "NULL argument");
+  DeviceGuard g(p->device);
+  if (p->dirty || p->ptrs_dirty) {
+    int rc = build_tables(p);
+    if (rc) return rc;
+  }
+  const int es = elem_size(p->dtype);
+  for (int l = 0; l < p->n_lanes; ++l) {
+    cudaStream_t st = (streams && n_streams > 0) ? (cudaStream_t)streams[l % n_streams] : (cudaStream_t)0;
+    const auto &rings = p->lanes[l].rings;
+    for (size_t i = 0; i < p->local.size(); ++i) {
+      const int pos = p->local[i];
+      for (int r : rings) {
+        if (p->rlen[r] == 0) continue;
+        const size_t off = (size_t)p->rstart[r] * es, bytes = (size_t)p->rlen[r] * es;
+        RV_CUDA(cudaMemcpyAsync((char *)p->src[pos] + off, (const char *)host_src[i] + off, bytes,
+                                cudaMemcpyHostToDevice, st));
+      }
+    }
+    int rc = launch_lane(p, l, st);
+    if (rc) return rc;
+    for (size_t i = 0; i < p->local.size(); ++i) {
+      const int pos = p->local[i];
+      for (int r : rings) {
+        if (p->rlen[r] == 0) continue;
+        const size_t off = (size_t)p->rstart[r] * es, bytes = (size_t)p->rlen[r] * es;
+        RV_CUDA(cudaMemcpyAsync((char *)host_dst[i] + off, (const char *)p->dst[pos] + off, bytes,
+                                cudaMemcpyDeviceToHost, st));
+      }
+    }
+  }
+  return RV_OK;
+}
+
+int rv_plan_status(rv_plan *p, char *diag, size_t diag_len) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  DeviceGuard g(p->device);
+  RV_CUDA(cudaDeviceSynchronize());
+  unsigned st[4] = {0, 0, 0, 0};
+  RV_CUDA(cudaMemcpy(st, p->status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st[0] == 0) {
+    if (diag && diag_len) snprintf(diag, diag_len, "no ring is stalled");
+    return RV_OK;
+  }
+  const unsigned phase = st[1] >> 16, lane = (st[1] >> 8) & 0xff, peer = st[1] & 0xff;
+  std::string rings;
+  if (lane < p->lanes.size())
+    for (int r : p->lanes[lane].rings) rings += (rings.empty() ? "" : "|") + std::to_string(r);
+  if (diag && diag_len)
+    snprintf(diag, diag_len, "waiting on: (ring=%s, phase=%s, rank=%u)", rings.empty() ? "?" : rings.c_str(),
+             phase == 0 ? "arrive" : "depart", peer);
+  return set_err(RV_E_TIMEOUT, "peer rank %u never reached the %s barrier (lane %u)", peer,
+                 phase == 0 ? "arrive" : "depart", lane);
+}
+
+int rv_plan_reset_status(rv_plan *p) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  DeviceGuard g(p->device);
+  RV_CUDA(cudaMemset(p->status, 0, 4 * sizeof(unsigned)));
+  RV_CUDA(cudaDeviceSynchronize());
+  return RV_OK;
+}
+
+int rv_plan_destroy(rv_plan *p) {
+  if (!p) return RV_OK;
+  {
+    DeviceGuard g(p->device);
+    free_lanes(p);
+    if (p->flags) cudaFree(p->flags);
+    if (p->states) cudaFree(p->states);
+    if (p->status) cudaFree(p->status);
+  }
+  delete p;
+  return RV_OK;
+}
+
+int rv_blend(int device, int dtype, void *live, const void *snap, const void *mean, int64_t n, void *stream) {
+  if (n < 0 || (n > 0 && (!live || !snap || !mean))) return set_err(RV_E_ARG, "bad blend arguments");
+  if (n == 0) return RV_OK;
+  DeviceGuard g(device);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool aligned = ((uintptr_t)live % 16 == 0) && ((uintptr_t)snap % 16 == 0) && ((uintptr_t)mean % 16 == 0);
+  const int es = elem_size(dtype);
+  const int N = 16 / es;
+  if (aligned && n >= N) {
+    const int64_t nvec = n / N;
+    const int grid = (int)std::min<int64_t>((nvec + kThreads - 1) / kThreads, (int64_t)sms * 8);
+    if (dtype == RV_DTYPE_F64)
+      blend_kernel_v4<double, unsigned long long><<<grid, kThreads, 0, st>>>(
+          (double *)live, (const double *)snap, (const double *)mean, nvec);
+    else
+      blend_kernel_v4<float, unsigned><<<grid, kThreads, 0, st>>>((float *)live, (const float *)snap,
+                                                                 (const float *)mean, nvec);
+    RV_CUDA(cudaGetLastError());
+    const int64_t done = nvec * N;
+    if (done < n) {
+      if (dtype == RV_DTYPE_F64)
+        blend_kernel<double, unsigned long long><<<1, kThreads, 0, st>>>(
+            (double *)live + done, (const double *)snap + done, (const double *)mean + done, n - done);
+      else
+        blend_kernel<float, unsigned><<<1, kThreads, 0, st>>>((float *)live + done, (const float *)snap + done,
+                                                             (const float *)mean + done, n - done);
+      RV_CUDA(cudaGetLastError());
+    }
+    return RV_OK;
+  }
+  const int grid = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, (int64_t)sms * 8);
+  if (dtype == RV_DTYPE_F64)
+    blend_kernel<double, unsigned long long><<<grid, kThreads, 0, st>>>((double *)live, (const double *)snap,
+                                                                       (const double *)mean, n);
+  else
+    blend_kernel<float, unsigned><<<grid, kThreads, 0, st>>>((float *)live, (const float *)snap,
+                                                            (const float *)mean, n);
+  RV_CUDA(cudaGetLastError());
+  return RV_OK;
+}
+
+int rv_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+int rv_ipc_export(const void *dev_ptr, void *handle_out, uint64_t *offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return set_err(RV_E_ARG, "NULL argument");
+  cudaPointerAttributes attr;
+  RV_CUDA(cudaPointerGetAttributes(&attr, dev_ptr));
+  if (attr.type != cudaMemoryTypeDevice) return set_err(RV_E_ARG, "pointer %p is not device memory", dev_ptr);
+  DeviceGuard g(attr.device);
+  unsigned long long base = 0;
+  int rc = alloc_base(dev_ptr, &base);
+  if (rc) return rc;
+  cudaIpcMemHandle_t h;
+  RV_CUDA(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  return RV_OK;
+}
+
+int rv_ipc_import(int device, const void *handle, uint64_t offset, void **dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return set_err(RV_E_ARG, "NULL argument");
+  DeviceGuard g(device);
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  auto key = std::make_pair(device, std::string((const char *)handle, sizeof(cudaIpcMemHandle_t)));
+  auto it = g_ipc.find(key);
+  void *base = nullptr;
+  if (it != g_ipc.end()) {
+    base = it->second.base;
+    it->second.refs++;
+  } else {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return set_err(RV_E_PEER_ACCESS, "cudaIpcOpenMemHandle failed: %s", cudaGetErrorString(e));
+    g_ipc[key] = IpcEntry{base, 1};
+  }
+  *dev_ptr_out = (char *)base + offset;
+  return RV_OK;
+}
+
+int rv_ipc_close(int device, void *dev_ptr) {
+  DeviceGuard g(device);
+  unsigned long long base = 0;
+  int rc = alloc_base(dev_ptr, &base);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (auto it = g_ipc.begin(); it != g_ipc.end(); ++it) {
+    if (it->first.first == device && it->second.base == (void *)(uintptr_t)base) {
+      if (--it->second.refs == 0) {
+        cudaIpcCloseMemHandle(it->second.base);
+        g_ipc.erase(it);
+      }
+      return RV_OK;
+    }
+  }
+  return set_err(RV_E_ARG, "pointer %p was not imported on device %d", dev_ptr, device);
+}
+
+int rv_enable_peer_access(int device, int peer) {
+  if (device == peer) return RV_OK;
+  int can = 0;
+  RV_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return set_err(RV_E_PEER_ACCESS, "device %d cannot access device %d", device, peer);
+  DeviceGuard g(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return RV_OK;
+  }
+  if (e != cudaSuccess)
+    return set_err(RV_E_PEER_ACCESS, "cudaDeviceEnablePeerAccess(%d->%d): %s", device, peer, cudaGetErrorString(e));
+  return RV_OK;
+}
+
+int rv_device_sm_count(int device) {
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return n;
+}
+
+}  // extern "C"

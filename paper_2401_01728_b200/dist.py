@@ -1,0 +1,153 @@
+"""One process per GPU: the multi-ring average across ranks of a torch.distributed group.
+
+Each rank hosts one cluster (its live parameter vector on its own GPU).  At
+construction the ranks exchange CUDA IPC handles of their parameter buffers
+and barrier-flag areas over torch.distributed (plumbing only; gloo or nccl),
+so every rank can address every peer's buffer over NVLink.  A cycle is then
+one kernel per rank with no host round trip and no NCCL call: rank k folds
+chunk k of every ring from all C buffers in ring order, divides by C, and
+stores the mean into all C buffers (multiring.py:302-333 arithmetic).
+
+Ring member order is ascending cluster id (multiring.py:95): ranks are sorted
+by the ``cluster_id`` they pass (default: their rank).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+from . import _native as N
+from .errors import ConfigError, LayoutError
+from .plan import DevicePlan, _dtype_code
+from .schedule import ring_arrays
+
+
+def _export(ptr: int) -> tuple[bytes, int]:
+    lib = N.load()
+    size = lib.rv_ipc_handle_size()
+    buf = ctypes.create_string_buffer(size)
+    off = ctypes.c_uint64()
+    N.check(lib.rv_ipc_export(ctypes.c_void_p(int(ptr)), buf, ctypes.byref(off)), "rv_ipc_export")
+    return buf.raw, int(off.value)
+
+
+def _import(device: int, handle: bytes, offset: int) -> int:
+    lib = N.load()
+    out = ctypes.c_void_p()
+    N.check(lib.rv_ipc_import(int(device), handle, ctypes.c_uint64(int(offset)), ctypes.byref(out)),
+            "rv_ipc_import")
+    return int(out.value)
+
+
+def _close(device: int, ptr: int) -> None:
+    N.load().rv_ipc_close(int(device), ctypes.c_void_p(int(ptr)))
+
+
+class DistRingGroup:
+    """Collective multi-ring averaging of one CUDA buffer per rank.
+
+    ``src`` is read and ``dst`` (default: ``src``, i.e. in place) written;
+    both must stay allocated while the group lives.  All ranks must call
+    ``average`` the same number of times in the same order, as with any
+    collective.
+    """
+
+    def __init__(self, schedule=None, src=None, dst=None, *, starts: Sequence[int] | None = None,
+                 lens: Sequence[int] | None = None, cluster_id: int | None = None, acc: str = "f64",
+                 lanes: int = 1, group=None, timeout_s: float | None = None):
+        import torch.distributed as dist
+
+        if src is None:
+            raise ConfigError("DistRingGroup needs the rank's parameter buffer")
+        if schedule is not None:
+            starts, lens = ring_arrays(schedule)
+            total = int(schedule.total_params)
+        else:
+            if starts is None or lens is None:
+                raise ConfigError("pass a schedule or ring starts/lens")
+            starts, lens = [int(s) for s in starts], [int(n) for n in lens]
+            total = sum(lens)
+        dst = src if dst is None else dst
+        for t in (src, dst):
+            if not t.is_cuda or not t.is_contiguous():
+                raise LayoutError("DistRingGroup buffers must be contiguous CUDA tensors")
+            if t.numel() != total:
+                raise LayoutError(f"buffer has {t.numel()} elements, schedule expects {total}")
+        if dst.dtype != src.dtype:
+            raise LayoutError("src and dst dtypes differ")
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world < 2:
+            raise ConfigError("all-reduce needs at least 2 clusters")
+        if self.world > N.RV_MAX_RANKS:
+            raise ConfigError(f"at most {N.RV_MAX_RANKS} ranks")
+        self.device = src.device.index
+        self.src, self.dst = src, dst
+        self.total = total
+        self.starts, self.lens = starts, lens
+        cid = self.rank if cluster_id is None else int(cluster_id)
+
+        self.plan = DevicePlan(self.device, self.world, starts, lens, total, _dtype_code(src.dtype), acc)
+        if lanes != 1:
+            self.plan.set_lanes(lanes)
+        if timeout_s is not None:
+            self.plan.set_timeout(timeout_s)
+        flag_ptr, _ = self.plan.flag_area()
+        mine = {
+            "cid": cid,
+            "src": _export(src.data_ptr()),
+            "dst": _export(dst.data_ptr()),
+            "flags": _export(flag_ptr),
+        }
+        everyone: list = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        cids = [e["cid"] for e in everyone]
+        if len(set(cids)) != len(cids):
+            raise ConfigError(f"duplicate cluster ids across ranks: {cids}")
+        order = sorted(range(self.world), key=lambda r: cids[r])  # position -> rank
+        self.position = order.index(self.rank)
+        self._imported: list[int] = []
+        areas = [0] * self.world
+        for pos, r in enumerate(order):
+            e = everyone[r]
+            if r == self.rank:
+                self.plan.bind(pos, src.data_ptr(), dst.data_ptr())
+                areas[pos] = flag_ptr
+                continue
+            s = _import(self.device, *e["src"])
+            d = s if e["dst"] == e["src"] else _import(self.device, *e["dst"])
+            f = _import(self.device, *e["flags"])
+            self._imported += [s, f] + ([d] if d != s else [])
+            self.plan.bind(pos, s, d)
+            areas[pos] = f
+        self.plan.set_local([self.position])
+        self.plan.set_peers(self.position, self.world, areas)
+        dist.barrier(group=group)
+
+    def average(self, streams=None) -> None:
+        """Launch one cycle on ``streams`` (default: the current stream)."""
+        import torch
+
+        st = streams if streams is not None else [torch.cuda.current_stream(self.device)]
+        st = st if isinstance(st, (list, tuple)) else [st]
+        self.plan.run(st)
+
+    def average_host(self, host_src, host_dst, streams=None) -> None:
+        """Cycle from/to pinned HOST tensors: H2D, average, D2H, pipelined
+        per lane (rv_allreduce_mean_host)."""
+        import torch
+
+        st = streams if streams is not None else [torch.cuda.current_stream(self.device)]
+        st = st if isinstance(st, (list, tuple)) else [st]
+        self.plan.run_host([host_src.data_ptr()], [host_dst.data_ptr()], st)
+
+    def check(self) -> None:
+        self.plan.check_status()
+
+    def close(self) -> None:
+        for p in self._imported:
+            _close(self.device, p)
+        self._imported = []
+        self.plan.close()
