@@ -221,6 +221,32 @@ def synth(total: int, key: int, device):
     return torch.randn(total, device=device, generator=g, dtype=torch.float32) * SIGMA
 
 
+def warm_under_load(step, warmup: int, seconds: float = 0.6, lockstep: bool = False):
+    """W untimed warm-up steps, extended until ~`seconds` of load so the clock
+    sampler (started just before) has samples under load.  With `lockstep`
+    (multi-rank) the step count is agreed across ranks: each rank runs the
+    same number of collective cycles."""
+    import torch
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    step()
+    torch.cuda.synchronize()
+    per = max(time.perf_counter() - t0, 1e-5)
+    extra = int(min(5000, seconds / per))
+    if lockstep:
+        import torch.distributed as dist
+
+        t = torch.tensor([extra])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        extra = int(t)
+    for _ in range(extra):
+        step()
+    torch.cuda.synchronize()
+
+
 def time_steps(fn, stream, steps: int):
     """Per-step CUDA-event durations (ms) on `stream`."""
     import torch
@@ -260,13 +286,10 @@ def run_single(args):
         else:
             g.run({0: [stream]})
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    g.check()
     clocks = ClockSampler(0)
     clocks.start()
-    torch.cuda.synchronize()
+    warm_under_load(step, args.warmup)
+    g.check()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
@@ -377,13 +400,11 @@ def run_multi(args, rank: int, world: int, local_rank: int):
         else:
             grp.average([stream])
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    grp.check()
     clocks = ClockSampler(local_rank) if rank == 0 else None
     if clocks:
         clocks.start()
+    warm_under_load(step, args.warmup, lockstep=True)
+    grp.check()
     dist.barrier()
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
@@ -506,7 +527,7 @@ def nccl_compare(lens, x, world: int, steps: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert")

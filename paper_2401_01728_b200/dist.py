@@ -44,6 +44,22 @@ def _close(device: int, ptr: int) -> None:
     N.load().rv_ipc_close(int(device), ctypes.c_void_p(int(ptr)))
 
 
+def rendezvous(mine: dict, group=None) -> tuple[list, list[int], int]:
+    """All-gather each rank's descriptor (cluster id + IPC handles) and order
+    ranks by ascending cluster id -- the ring member order (multiring.py:95).
+    Returns (descriptors by rank, rank of each position, this rank's position)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    everyone: list = [None] * world
+    dist.all_gather_object(everyone, mine, group=group)
+    cids = [e["cid"] for e in everyone]
+    if len(set(cids)) != len(cids):
+        raise ConfigError(f"duplicate cluster ids across ranks: {cids}")
+    order = sorted(range(world), key=lambda r: cids[r])
+    return everyone, order, order.index(dist.get_rank(group))
+
+
 class DistRingGroup:
     """Collective multi-ring averaging of one CUDA buffer per rank.
 
@@ -101,13 +117,7 @@ class DistRingGroup:
             "dst": _export(dst.data_ptr()),
             "flags": _export(flag_ptr),
         }
-        everyone: list = [None] * self.world
-        dist.all_gather_object(everyone, mine, group=group)
-        cids = [e["cid"] for e in everyone]
-        if len(set(cids)) != len(cids):
-            raise ConfigError(f"duplicate cluster ids across ranks: {cids}")
-        order = sorted(range(self.world), key=lambda r: cids[r])  # position -> rank
-        self.position = order.index(self.rank)
+        everyone, order, self.position = rendezvous(mine, group)
         self._imported: list[int] = []
         areas = [0] * self.world
         for pos, r in enumerate(order):

@@ -1,0 +1,99 @@
+"""Multi-process parity worker (one process per GPU), launched by
+tests/test_dist_gpu.py through torchrun.  Every rank builds the same seeded
+inputs for all C = world clusters, averages its own through DistRingGroup,
+and checks its result bitwise against the oracle."""
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import ring_oracle  # noqa: E402
+from paper_2401_01728_b200.dist import DistRingGroup  # noqa: E402
+
+
+def bits(a):
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    os.environ.setdefault("RAVNEST_B200_TIMEOUT_S", "10")
+    cases = []
+    rng = np.random.Generator(np.random.Philox(key=77))
+    for i in range(6):
+        n_rings = int(rng.integers(1, 9))
+        lens = [int(x) for x in rng.integers(0, 200000, n_rings)]
+        lens[0] += world - 1
+        cases.append(lens)
+    cases.append([1, 0, 2, world + 1, 3 * world - 1])      # tiny and zero-length rings
+    cases.append([26201088, 27168768, 27170304, 28942080])  # BERT-base rings
+    failures = 0
+    for ci, lens in enumerate(cases):
+        total = sum(lens)
+        starts = list(np.cumsum([0] + lens[:-1]))
+        big = total > 10_000_000
+        variants = [("f64", torch.float32, 1, False, False)] if big else [
+            ("f64", torch.float32, 1, False, False),
+            ("native", torch.float32, 1, True, False),
+            ("f64", torch.float64, 1, False, True),
+            ("f64", torch.float32, len(lens), False, False),
+            ("f64", torch.float32, 1, False, True),
+        ]
+        for acc, dt, lanes, reverse_ids, src_ne_dst in variants:
+            npdt = np.float32 if dt == torch.float32 else np.float64
+            xs = [np.random.Generator(np.random.Philox(key=1000 * ci + m)).normal(0, 1, total).astype(npdt)
+                  for m in range(world)]
+            cid = (world - 1 - rank) if reverse_ids else rank
+            order = sorted(range(world), key=lambda r: (world - 1 - r) if reverse_ids else r)
+            vals = [xs[r] for r in order]  # ascending cluster id
+            want = ring_oracle.ring_mean(starts, lens, vals, acc=acc)[order.index(rank)].astype(npdt)
+            off = 1 if src_ne_dst else 0
+            buf = torch.empty(total + off + 4, dtype=dt, device=f"cuda:{local}")
+            x = buf[off:off + total]
+            x.copy_(torch.from_numpy(xs[rank]))
+            dst = torch.full((total,), float("nan"), dtype=dt, device=f"cuda:{local}") if src_ne_dst else None
+            g = DistRingGroup(src=x, dst=dst, starts=starts, lens=lens, cluster_id=cid, acc=acc, lanes=lanes)
+            streams = [torch.cuda.Stream() for _ in range(lanes)]
+            for s in streams:
+                s.wait_stream(torch.cuda.current_stream())
+            g.average(streams)
+            torch.cuda.synchronize()
+            g.check()
+            got = (dst if dst is not None else x).cpu().numpy()
+            if not np.array_equal(bits(got), bits(want)):
+                bad = int(np.sum(bits(got) != bits(want)))
+                print(f"rank {rank} case {ci} {acc} {dt} lanes={lanes} rev={reverse_ids}: {bad} mismatches",
+                      flush=True)
+                failures += 1
+            if not big and not src_ne_dst and lanes == 1:
+                # host-buffer path, twice in a row (epochs advance consistently)
+                h_in = torch.from_numpy(xs[rank]).pin_memory()
+                h_out = torch.empty_like(h_in).pin_memory()
+                for _ in range(2):
+                    g.average_host(h_in, h_out)
+                    torch.cuda.synchronize()
+                g.check()
+                if not np.array_equal(bits(h_out.numpy()), bits(want)):
+                    print(f"rank {rank} case {ci} host path mismatch", flush=True)
+                    failures += 1
+            dist.barrier()
+            g.close()
+    t = torch.tensor([failures])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"DIST {'OK' if int(t) == 0 else 'FAIL'} world={world} cases={len(cases)} failures={int(t)}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if int(t) == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,59 @@
+"""World-size-2 gloo tests on CPU for the multi-process host logic: the
+rendezvous that orders ranks by cluster id, and duplicate-id rejection."""
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cids, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_01728_b200.dist import rendezvous
+    from paper_2401_01728_b200.errors import ConfigError
+
+    try:
+        everyone, order, pos = rendezvous({"cid": cids[rank], "src": (b"h%d" % rank, 16 * rank)})
+        q.put((rank, [e["cid"] for e in everyone], order, pos, everyone[order[0]]["src"]))
+    except ConfigError as e:
+        q.put((rank, "ConfigError", str(e)))
+    dist.destroy_process_group()
+
+
+def _run(world, cids):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cids, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    return sorted(out, key=lambda t: t[0])
+
+
+def test_rendezvous_orders_by_cluster_id():
+    out = _run(2, [7, 3])
+    for rank, cids, order, pos, first_src in out:
+        assert cids == [7, 3]
+        assert order == [1, 0]          # position 0 = cluster 3 = rank 1
+        assert pos == (1 if rank == 0 else 0)
+        assert first_src == (b"h1", 16)
+
+
+def test_rendezvous_rejects_duplicate_ids():
+    out = _run(2, [5, 5])
+    assert all(o[1] == "ConfigError" for o in out)
