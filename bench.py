@@ -386,7 +386,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     dev = torch.device(f"cuda:{local_rank}")
     torch.cuda.set_device(dev)
     x = synth(total, rank, dev)
-    grp = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes)
+    grp = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes,
+                        protocol=args.protocol)
     stream = torch.cuda.current_stream()
     lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
 
@@ -425,7 +426,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     # e2e through the host-buffer C ABI: pinned host -> GPU -> average -> host
     hsrc = x.cpu().pin_memory()
     hdst = torch.empty_like(hsrc).pin_memory()
-    grp_e2e = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=len(lens))
+    grp_e2e = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=len(lens),
+                            protocol=args.protocol)
     e2e_streams = [torch.cuda.Stream() for _ in lens]
 
     def e2e_step():
@@ -470,7 +472,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
             "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
             "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
-                       "placement": "one cluster per GPU", "lanes": args.lanes,
+                       "placement": "one cluster per GPU", "lanes": args.lanes, "protocol": args.protocol,
                        "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
                        "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
@@ -533,6 +535,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert")
     ap.add_argument("--acc", choices=["f64", "native"], default="f64")
     ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--protocol", choices=["pull", "push"], default="pull")
     ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")
     ap.add_argument("--cpu-sample-params", type=int, default=8_000_000)
     ap.add_argument("--nccl", type=int, default=1)

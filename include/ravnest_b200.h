@@ -61,6 +61,17 @@ extern "C" {
 #define RV_ACC_F64 0
 #define RV_ACC_NATIVE 1
 
+/* Transport protocols for multi-device plans.
+ * RV_PROTO_PULL: the owner of chunk k loads chunk k of every member over
+ *   NVLink, folds, and stores the mean into every member (arrive + depart
+ *   barriers).
+ * RV_PROTO_PUSH: NVLink carries stores only -- each member stores its copy of
+ *   chunk k into owner k's staging slot (one release flag per 256 KB unit),
+ *   the owner folds from local memory and stores the mean into every member
+ *   (depart barrier only).  Needs one position per rank, rank == position. */
+#define RV_PROTO_PULL 0
+#define RV_PROTO_PUSH 1
+
 typedef struct rv_plan rv_plan;
 
 int rv_version(void);
@@ -92,6 +103,14 @@ int rv_plan_flag_area(rv_plan *plan, void **flags, size_t *bytes);
 /* Multi-device group: this plan is `rank` of `n_ranks`; peer_flag_areas[r] is
  * rank r's flag area mapped into this device (entry `rank` is ignored). */
 int rv_plan_set_peers(rv_plan *plan, int rank, int n_ranks, void *const *peer_flag_areas);
+
+int rv_plan_set_protocol(rv_plan *plan, int proto);
+
+/* Push protocol: this plan's staging + unit-flag area (allocated on first
+ * call, sized from the schedule and lane count; IPC-exportable).  Every rank
+ * passes all ranks' areas (indexed by rank, mapped into this device). */
+int rv_plan_push_area(rv_plan *plan, void **area, size_t *bytes);
+int rv_plan_set_push_peers(rv_plan *plan, void *const *areas);
 
 int rv_plan_set_timeout(rv_plan *plan, double seconds);
 

@@ -27,6 +27,9 @@ RV_DTYPE_F64 = 1
 RV_ACC_F64 = 0
 RV_ACC_NATIVE = 1
 
+RV_PROTO_PULL = 0
+RV_PROTO_PUSH = 1
+
 RV_MAX_CLUSTERS = 16
 RV_MAX_RANKS = 16
 
@@ -45,6 +48,9 @@ SIGNATURES = {
     "rv_plan_set_lanes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rv_plan_flag_area": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, ctypes.POINTER(ctypes.c_size_t)]),
     "rv_plan_set_peers": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _c_void_pp]),
+    "rv_plan_set_protocol": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "rv_plan_push_area": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, ctypes.POINTER(ctypes.c_size_t)]),
+    "rv_plan_set_push_peers": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp]),
     "rv_plan_set_timeout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double]),
     "rv_allreduce_mean": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, ctypes.c_int]),
     "rv_allreduce_mean_host": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, _c_void_pp, _c_void_pp, ctypes.c_int]),

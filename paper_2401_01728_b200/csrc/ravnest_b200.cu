@@ -74,11 +74,14 @@ struct DeviceGuard {
 
 constexpr int kThreads = 256;
 constexpr unsigned kStatusTimeout = 1u;
+constexpr int64_t kUnitBytes = 256 * 1024;  // push protocol: bytes per flagged unit
 
 struct Seg {
   int64_t lo, hi;            // chunk [lo, hi) in elements
   int64_t body_lo, body_hi;  // 16-byte aligned vector body inside it
-  int32_t k;                 // fold start position (chunk index in its ring)
+  int64_t stage_off;         // push: element offset of this chunk in the owner's staging slot
+  int64_t unit0;             // push: first unit index of this chunk (per owner, per lane)
+  int32_t k;                 // fold start position = owner position (chunk index in its ring)
   int32_t ring;
 };
 
@@ -92,21 +95,34 @@ struct LaneState {
 struct CycleParams {
   const void *src[RV_MAX_CLUSTERS];
   void *dst[RV_MAX_CLUSTERS];
-  unsigned long long *peer_flags[RV_MAX_RANKS];  // rank r's flag area (as mapped here)
-  const Seg *segs;
-  const int64_t *tile_prefix;  // nseg + 1 entries
+  void *stage[RV_MAX_CLUSTERS];                 // push: owner q's staging area (as mapped here)
+  unsigned long long *pflags[RV_MAX_CLUSTERS];  // push: owner q's unit flags (as mapped here)
+  unsigned long long *peer_flags[RV_MAX_RANKS]; // rank r's barrier flag area (as mapped here)
+  const Seg *segs;             // pull: this device's chunks; push: every owner's, owner-major
+  const int64_t *tile_prefix;  // pull: nseg + 1 entries
   unsigned long long *my_flags;
   LaneState *state;
-  unsigned int *status;  // [0] code, [1] diag
-  int64_t n_tiles;
+  unsigned int *status;        // [0] code, [1] diag
+  int64_t n_tiles;             // pull
+  int64_t stride;              // push: staging elements per writer slot
+  int64_t units_max;           // push: unit-flag slots per (lane, writer)
+  int64_t scatter_umax;        // push: max units over the other owners
+  int64_t unit_vecs;           // push: vectors per unit
+  int64_t ounits[RV_MAX_CLUSTERS];
+  int oseg_base[RV_MAX_CLUSTERS + 1];
   unsigned long long timeout_ns;
   double inv_c;
-  int C, nseg, rank, n_ranks, lane, pow2;
+  int C, nseg, rank, n_ranks, lane, pow2, me;
 };
 
-// flag slot of (lane, sender rank, phase) inside a receiver's flag area
+// flag slot of (lane, sender rank, phase) inside a receiver's barrier area
 __host__ __device__ inline size_t flag_index(int lane, int sender, int phase) {
   return ((size_t)lane * RV_MAX_RANKS + (size_t)sender) * 2 + (size_t)phase;
+}
+
+// push: flag slot of (lane, writer, unit) inside an owner's unit-flag area
+__host__ __device__ inline size_t pflag_index(int lane, int c, int writer, int64_t units_max, int64_t u) {
+  return ((size_t)lane * c + (size_t)writer) * (size_t)units_max + (size_t)u;
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -125,23 +141,30 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
-// Wait until every peer posted `phase` for epoch e.  Returns false on timeout.
+// Spin until *f >= e.  Returns false on timeout (status set, diag recorded)
+// or when another block already failed.
+__device__ bool wait_flag(const CycleParams &p, const unsigned long long *f, unsigned long long e,
+                          unsigned long long t0, unsigned diag) {
+  unsigned spins = 0;
+  while (ld_acquire_sys(f) < e) {
+    if ((++spins & 255u) == 0) {
+      if (*(volatile unsigned *)p.status != 0) return false;
+      if (globaltimer() - t0 > p.timeout_ns) {
+        if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u) p.status[1] = diag;
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+// Wait until every peer posted `phase` for epoch e.
 __device__ bool wait_peers(const CycleParams &p, int phase, unsigned long long e) {
   const unsigned long long t0 = globaltimer();
   for (int r = 0; r < p.n_ranks; ++r) {
     if (r == p.rank) continue;
-    const unsigned long long *f = p.my_flags + flag_index(p.lane, r, phase);
-    unsigned spins = 0;
-    while (ld_acquire_sys(f) < e) {
-      if ((++spins & 255u) == 0) {
-        if (*(volatile unsigned *)p.status != 0) return false;
-        if (globaltimer() - t0 > p.timeout_ns) {
-          if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u)
-            p.status[1] = ((unsigned)phase << 16) | ((unsigned)p.lane << 8) | (unsigned)r;
-          return false;
-        }
-      }
-    }
+    const unsigned diag = ((unsigned)phase << 16) | ((unsigned)p.lane << 8) | (unsigned)r;
+    if (!wait_flag(p, p.my_flags + flag_index(p.lane, r, phase), e, t0, diag)) return false;
   }
   return true;
 }
@@ -150,6 +173,25 @@ __device__ void post_peers(const CycleParams &p, int phase, unsigned long long e
   for (int r = 0; r < p.n_ranks; ++r) {
     if (r == p.rank) continue;
     st_release_sys(p.peer_flags[r] + flag_index(p.lane, p.rank, phase), e);
+  }
+}
+
+// Exit barrier: the last block of this launch tells every peer that all of
+// this device's stores (local and remote) are done, then waits for theirs,
+// so nobody resumes training on a buffer a peer is still writing.
+__device__ void depart(const CycleParams &p, unsigned long long epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned prev = atomicAdd(&p.state->done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      post_peers(p, 1, epoch);
+      if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
+      p.state->done = 0u;
+      *(volatile unsigned long long *)&p.state->epoch = epoch;
+      __threadfence();
+    }
   }
 }
 
@@ -182,26 +224,83 @@ __device__ __forceinline__ T finish(Acc acc, const CycleParams &p) {
   return (T)q;
 }
 
-// Scalar fold of element i (chunk edges and misaligned buffers).
-template <typename T, typename Acc>
-__device__ __forceinline__ void fold_scalar(const CycleParams &p, int k, int64_t i) {
-  int m = k;
-  Acc acc = (Acc)__ldcs(static_cast<const T *>(p.src[m]) + i);
+// Element i of member m as this device reads it.  Pull: the member's own
+// buffer (local or peer).  Push: the owner's own buffer for m == me, else the
+// staging slot member m pushed into.
+template <typename T, bool PUSH>
+__device__ __forceinline__ const T *member_elem(const CycleParams &p, const Seg &s, int m, int64_t i) {
+  if (!PUSH || m == p.me) return static_cast<const T *>(p.src[m]) + i;
+  return static_cast<const T *>(p.stage[p.me]) + ((int64_t)m * p.stride + s.stage_off + (i - s.lo));
+}
+
+// Fold of one element (chunk edges, misaligned buffers): ring order from s.k.
+template <typename T, typename Acc, bool PUSH>
+__device__ __forceinline__ void fold_scalar(const CycleParams &p, const Seg &s, int64_t i) {
+  int m = s.k;
+  Acc acc = (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
   for (int q = 1; q < p.C; ++q) {
     m = (m + 1 == p.C) ? 0 : m + 1;
-    acc = acc + (Acc)__ldcs(static_cast<const T *>(p.src[m]) + i);
+    acc = acc + (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
   }
   const T out = finish<T, Acc>(acc, p);
   for (int q = 0; q < p.C; ++q) __stcs(static_cast<T *>(p.dst[q]) + i, out);
 }
 
-// CB: compile-time capacity for C (2/4/8/16), VB: vector bytes, U: vectors
-// per thread per tile.  U*CB independent loads are in flight per thread.
+// Fold vectors [jbeg, jend) of chunk s: every thread takes U vectors per
+// pass, loads all C members of each (U*C loads in flight), folds in ring
+// order, divides, and stores the mean into all C member buffers.
+template <typename T, typename Acc, int CB, int VB, int U, bool PUSH>
+__device__ __forceinline__ void fold_range(const CycleParams &p, const Seg &s, int64_t jbeg, int64_t jend) {
+  constexpr int N = VB / sizeof(T);
+  using Raw = typename RawVec<VB>::type;
+  for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * U) {
+    Lanes<T, VB> x[U][CB];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + (int64_t)u * kThreads;
+      if (j < jend) {
+        const int64_t i = s.body_lo + j * N;
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          if (q < p.C) {
+            int m = s.k + q;
+            if (m >= p.C) m -= p.C;
+            x[u][q].raw = __ldcs(reinterpret_cast<const Raw *>(member_elem<T, PUSH>(p, s, m, i)));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + (int64_t)u * kThreads;
+      if (j < jend) {
+        Lanes<T, VB> out;
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          Acc acc = (Acc)x[u][0].v[e];
+#pragma unroll
+          for (int q = 1; q < CB; ++q)
+            if (q < p.C) acc = acc + (Acc)x[u][q].v[e];
+          out.v[e] = finish<T, Acc>(acc, p);
+        }
+        const int64_t i = s.body_lo + j * N;
+#pragma unroll
+        for (int q = 0; q < CB; ++q)
+          if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pull protocol: the owner of chunk k reads chunk k of every member (local
+// HBM or NVLink peer loads) and pushes the mean into every member.  Arrive
+// barrier first (peers' inputs final), depart barrier last.
+
 template <typename T, typename Acc, int CB, int VB, int U>
 __global__ void __launch_bounds__(kThreads)
 ring_cycle_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = VB / sizeof(T);
-  using Raw = typename RawVec<VB>::type;
   __shared__ int s_go;
   unsigned long long epoch = 0;
 
@@ -236,69 +335,128 @@ ring_cycle_kernel(const __grid_constant__ CycleParams p) {
       const Seg s = p.segs[a];
       const int64_t local_tile = t - __ldg(p.tile_prefix + a);
       const int64_t nvec = (s.body_hi - s.body_lo) / N;
-      const int64_t j0 = local_tile * tile_vecs + threadIdx.x;
-
-      Lanes<T, VB> x[U][CB];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + (int64_t)u * kThreads;
-        if (j < nvec) {
-          const int64_t off = s.body_lo + j * N;
-#pragma unroll
-          for (int q = 0; q < CB; ++q) {
-            if (q < p.C) {
-              int m = s.k + q;
-              if (m >= p.C) m -= p.C;
-              x[u][q].raw = __ldcs(reinterpret_cast<const Raw *>(static_cast<const T *>(p.src[m]) + off));
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + (int64_t)u * kThreads;
-        if (j < nvec) {
-          Lanes<T, VB> out;
-#pragma unroll
-          for (int e = 0; e < N; ++e) {
-            Acc acc = (Acc)x[u][0].v[e];
-#pragma unroll
-            for (int q = 1; q < CB; ++q)
-              if (q < p.C) acc = acc + (Acc)x[u][q].v[e];
-            out.v[e] = finish<T, Acc>(acc, p);
-          }
-          const int64_t off = s.body_lo + j * N;
-#pragma unroll
-          for (int q = 0; q < CB; ++q)
-            if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + off), out.raw);
-        }
-      }
+      const int64_t jbeg = local_tile * tile_vecs;
+      fold_range<T, Acc, CB, VB, U, false>(p, s, jbeg, min(nvec, jbeg + tile_vecs));
       if (local_tile == 0) {
         const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
         if ((int64_t)threadIdx.x < nhead + ntail) {
           const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
                                                           : s.body_hi + ((int64_t)threadIdx.x - nhead);
-          fold_scalar<T, Acc>(p, s.k, i);
+          fold_scalar<T, Acc, false>(p, s, i);
         }
       }
     }
   }
+  if (p.n_ranks > 1) depart(p, epoch);
+}
 
-  if (p.n_ranks > 1) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();  // this block's peer stores before the count
-      const unsigned prev = atomicAdd(&p.state->done, 1u);
-      if (prev == gridDim.x - 1) {
-        __threadfence_system();  // every block's stores are ordered before the post
-        post_peers(p, 1, epoch);
-        if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
-        p.state->done = 0u;
-        *(volatile unsigned long long *)&p.state->epoch = epoch;
-        __threadfence();
+// ---------------------------------------------------------------------------
+// push protocol (one position per rank, rank == position): NVLink carries
+// stores only.  Scatter: this rank copies its chunk-q slice of every ring into
+// owner q's staging slot and raises one release flag per 256 KB unit.  Fold:
+// for its own chunk, once every writer's flag for a unit is up, the owner
+// folds its own values and the staged ones in ring order and pushes the mean
+// into all members.  No arrive barrier is needed: a member's chunk reaches
+// the owner only after its kernel started (inputs final), and the owner
+// writes a member's buffer only after receiving that member's data for the
+// same unit.  The depart barrier still closes the cycle.
+
+template <typename T>
+__device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
+  int a = 0, b = nseg - 1;
+  while (a < b) {
+    const int mid = (a + b + 1) >> 1;
+    if (segs[mid].unit0 <= u) a = mid; else b = mid - 1;
+  }
+  return segs[a];
+}
+
+template <typename T, typename Acc, int CB, int VB, int U>
+__global__ void __launch_bounds__(kThreads)
+ring_push_kernel(const __grid_constant__ CycleParams p) {
+  constexpr int N = VB / sizeof(T);
+  constexpr int KC = (U * CB) < 16 ? (U * CB) : 16;  // vectors in flight per thread when copying
+  using Raw = typename RawVec<VB>::type;
+  __shared__ int s_ok;
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) {
+    s_epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
+    s_ok = (*(volatile unsigned *)p.status == 0);
+  }
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const int C = p.C, me = p.me;
+  const int64_t n_scatter = (int64_t)(C - 1) * p.scatter_umax;
+  const int64_t n_work = n_scatter + p.ounits[me];
+  const unsigned long long t0 = globaltimer();
+
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    if (!s_ok) break;
+    if (w < n_scatter) {
+      const int r = (int)(w % (C - 1));
+      const int64_t u = w / (C - 1);
+      int q = me + 1 + r;
+      if (q >= C) q -= C;
+      if (u >= p.ounits[q]) continue;
+      const Seg s = find_unit<T>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
+      const int64_t uu = u - s.unit0;
+      const int64_t nvec = (s.body_hi - s.body_lo) / N;
+      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
+      const T *src = static_cast<const T *>(p.src[me]);
+      T *stg = static_cast<T *>(p.stage[q]) + ((int64_t)me * p.stride + s.stage_off - s.lo);
+      for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * KC) {
+        Raw v[KC];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const int64_t j = j0 + (int64_t)c * kThreads;
+          if (j < jend) v[c] = __ldcs(reinterpret_cast<const Raw *>(src + s.body_lo + j * N));
+        }
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const int64_t j = j0 + (int64_t)c * kThreads;
+          if (j < jend) __stcs(reinterpret_cast<Raw *>(stg + s.body_lo + j * N), v[c]);
+        }
       }
+      if (uu == 0) {
+        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+        if ((int64_t)threadIdx.x < nhead + ntail) {
+          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
+                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
+          stg[i] = src[i];
+        }
+      }
+      __threadfence_system();  // this thread's stores, before the unit flag
+      __syncthreads();
+      if (threadIdx.x == 0)
+        st_release_sys(p.pflags[q] + pflag_index(p.lane, C, me, p.units_max, u), epoch);
+    } else {
+      const int64_t u = w - n_scatter;
+      const Seg s = find_unit<T>(p.segs + p.oseg_base[me], p.oseg_base[me + 1] - p.oseg_base[me], u);
+      if (threadIdx.x == 0) {
+        for (int m = 0; m < C && s_ok; ++m) {
+          if (m == me) continue;
+          const unsigned diag = (2u << 16) | ((unsigned)p.lane << 8) | (unsigned)m;
+          if (!wait_flag(p, p.pflags[me] + pflag_index(p.lane, C, m, p.units_max, u), epoch, t0, diag)) s_ok = 0;
+        }
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      const int64_t uu = u - s.unit0;
+      const int64_t nvec = (s.body_hi - s.body_lo) / N;
+      const int64_t jbeg = uu * p.unit_vecs;
+      fold_range<T, Acc, CB, VB, U, true>(p, s, jbeg, min(nvec, jbeg + p.unit_vecs));
+      if (uu == 0) {
+        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+        if ((int64_t)threadIdx.x < nhead + ntail) {
+          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
+                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
+          fold_scalar<T, Acc, true>(p, s, i);
+        }
+      }
+      __syncthreads();  // s_ok is re-armed by thread 0 for the next unit
     }
   }
+  depart(p, epoch);
 }
 
 // live <- mean + (live - snap); exactly mean where live == snap bitwise.
@@ -344,19 +502,19 @@ using KernelFn = void (*)(CycleParams);
 enum Mode { kF32Acc64 = 0, kF32Native = 1, kF64 = 2 };
 
 template <typename T, typename Acc, int VB>
-KernelFn pick_cb(int c) {
-  if (c <= 2) return ring_cycle_kernel<T, Acc, 2, VB, 8>;
-  if (c <= 4) return ring_cycle_kernel<T, Acc, 4, VB, 4>;
-  if (c <= 8) return ring_cycle_kernel<T, Acc, 8, VB, 2>;
-  return ring_cycle_kernel<T, Acc, 16, VB, 1>;
+KernelFn pick_cb(int c, bool push) {
+  if (c <= 2) return push ? ring_push_kernel<T, Acc, 2, VB, 8> : ring_cycle_kernel<T, Acc, 2, VB, 8>;
+  if (c <= 4) return push ? ring_push_kernel<T, Acc, 4, VB, 4> : ring_cycle_kernel<T, Acc, 4, VB, 4>;
+  if (c <= 8) return push ? ring_push_kernel<T, Acc, 8, VB, 2> : ring_cycle_kernel<T, Acc, 8, VB, 2>;
+  return push ? ring_push_kernel<T, Acc, 16, VB, 1> : ring_cycle_kernel<T, Acc, 16, VB, 1>;
 }
 
-KernelFn pick_kernel(int mode, int c, bool vec, int *u_out) {
+KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
   *u_out = c <= 2 ? 8 : c <= 4 ? 4 : c <= 8 ? 2 : 1;
   switch (mode) {
-    case kF32Acc64: return vec ? pick_cb<float, double, 16>(c) : pick_cb<float, double, 4>(c);
-    case kF32Native: return vec ? pick_cb<float, float, 16>(c) : pick_cb<float, float, 4>(c);
-    default: return vec ? pick_cb<double, double, 16>(c) : pick_cb<double, double, 8>(c);
+    case kF32Acc64: return vec ? pick_cb<float, double, 16>(c, push) : pick_cb<float, double, 4>(c, push);
+    case kF32Native: return vec ? pick_cb<float, float, 16>(c, push) : pick_cb<float, float, 4>(c, push);
+    default: return vec ? pick_cb<double, double, 16>(c, push) : pick_cb<double, double, 8>(c, push);
   }
 }
 
@@ -397,6 +555,7 @@ struct rv_plan {
   int C = 0, R = 0;
   int64_t total = 0;
   int dtype = RV_DTYPE_F32, acc = RV_ACC_F64;
+  int proto = RV_PROTO_PULL;
   std::vector<int64_t> rstart, rlen;
   std::vector<const void *> src;
   std::vector<void *> dst;
@@ -411,8 +570,14 @@ struct rv_plan {
   unsigned int *status = nullptr;
   unsigned long long timeout_ns = 20ull * 1000000000ull;
   int sm_count = 0;
+  // push protocol: [unit flags | staging] in one IPC-exportable allocation
+  char *push_area = nullptr;
+  size_t push_bytes = 0, pflag_bytes = 0;
+  int64_t stride_bound = 0, units_max = 0;
+  int push_lanes = 0;
+  std::vector<char *> peer_push;  // by rank
   // built lane tables
-  bool dirty = true;       // local positions / lanes / peers changed
+  bool dirty = true;       // local positions / lanes / peers / protocol changed
   bool ptrs_dirty = true;  // buffers rebound: rebuild only if the alignment class changed
   int built_vec = -1;
   int64_t built_a0 = -1;
@@ -424,10 +589,15 @@ struct rv_plan {
     int64_t elems = 0;
     std::vector<int> rings;
     int grid = 0;
+    // push
+    int64_t stride = 0, unit_vecs = 0, scatter_umax = 0;
+    std::vector<int64_t> ounits;
+    std::vector<int> oseg_base;
   };
   std::vector<Lane> lanes;
   KernelFn kernel = nullptr;
   int occ = 0;
+  bool use_push = false;
 };
 
 namespace {
@@ -441,6 +611,61 @@ void free_lanes(rv_plan *p) {
 }
 
 int elem_size(int dtype) { return dtype == RV_DTYPE_F64 ? 8 : 4; }
+
+// chunk bounds of ring r (multiring.py:134-144)
+std::vector<std::pair<int64_t, int64_t>> ring_chunks(const rv_plan *p, int r) {
+  std::vector<std::pair<int64_t, int64_t>> b(p->C);
+  const int64_t base = p->rlen[r] / p->C, rem = p->rlen[r] % p->C;
+  int64_t lo = p->rstart[r];
+  for (int k = 0; k < p->C; ++k) {
+    const int64_t n = base + (k < rem ? 1 : 0);
+    b[k] = {lo, lo + n};
+    lo += n;
+  }
+  return b;
+}
+
+// vector body of [lo, hi): element i is 16-byte aligned iff (i + a0) % N == 0
+void set_body(Seg &s, int N, int64_t a0) {
+  int64_t blo = s.lo + ((N - (s.lo + a0) % N) % N);
+  int64_t bhi = s.hi - ((s.hi + a0) % N);
+  if (bhi <= blo) blo = bhi = s.hi;  // no aligned vector: all edge elements (< 2N)
+  s.body_lo = blo;
+  s.body_hi = bhi;
+}
+
+bool push_active(const rv_plan *p) { return p->proto == RV_PROTO_PUSH && p->n_ranks > 1; }
+
+// Upper bounds of the push layout, from the schedule alone (before any
+// pointer is known): staging elements per writer slot, unit flags per lane.
+void push_bounds(const rv_plan *p, int64_t *stride_bound, int64_t *units_max) {
+  const int es = elem_size(p->dtype);
+  const int64_t nmax = 16 / es, unit_elems = kUnitBytes / es;
+  int64_t stride = nmax;
+  int64_t umax = 1;
+  for (int l = 0; l < p->n_lanes; ++l) {
+    int64_t u = 0;
+    for (int r = l; r < p->R; r += p->n_lanes) {
+      const int64_t chunk = (p->rlen[r] + p->C - 1) / p->C;
+      u += (chunk + unit_elems - 1) / unit_elems + 1;
+    }
+    umax = std::max(umax, u);
+  }
+  for (int r = 0; r < p->R; ++r) stride += (p->rlen[r] + p->C - 1) / p->C + 2 * nmax;
+  *stride_bound = stride;
+  *units_max = umax;
+}
+
+int upload(rv_plan::Lane &lane, const std::vector<Seg> &segs, const std::vector<int64_t> &prefix) {
+  if (segs.empty()) return RV_OK;
+  RV_CUDA(cudaMalloc(&lane.segs, sizeof(Seg) * segs.size()));
+  RV_CUDA(cudaMemcpy(lane.segs, segs.data(), sizeof(Seg) * segs.size(), cudaMemcpyHostToDevice));
+  if (!prefix.empty()) {
+    RV_CUDA(cudaMalloc(&lane.prefix, sizeof(int64_t) * prefix.size()));
+    RV_CUDA(cudaMemcpy(lane.prefix, prefix.data(), sizeof(int64_t) * prefix.size(), cudaMemcpyHostToDevice));
+  }
+  return RV_OK;
+}
 
 int build_tables(rv_plan *p) {
   for (int i = 0; i < p->C; ++i)
@@ -456,82 +681,124 @@ int build_tables(rv_plan *p) {
     if ((uintptr_t)p->src[i] % 16 != a || (uintptr_t)p->dst[i] % 16 != a) vec = false;
   }
   const int N = vec ? 16 / es : 1;
-  const int64_t a0 = vec ? (int64_t)(a / es) : 0;  // element i is vector aligned iff (i + a0) % N == 0
+  const int64_t a0 = vec ? (int64_t)(a / es) : 0;
   p->ptrs_dirty = false;
   if (!p->dirty && p->built_vec == (int)vec && p->built_a0 == a0) return RV_OK;
   p->built_vec = (int)vec;
   p->built_a0 = a0;
+  const bool push = push_active(p);
+  if (push) {
+    if (p->n_ranks != p->C || p->local.size() != 1 || p->local[0] != p->rank)
+      return set_err(RV_E_CONFIG, "push protocol needs one position per rank with rank == position");
+    if (!p->push_area || p->push_lanes != p->n_lanes)
+      return set_err(RV_E_ARG, "push area not allocated for %d lanes (call rv_plan_push_area)", p->n_lanes);
+    for (int r = 0; r < p->n_ranks; ++r)
+      if (!p->peer_push[r]) return set_err(RV_E_ARG, "push area of rank %d missing", r);
+  }
+  p->use_push = push;
   const int mode = p->dtype == RV_DTYPE_F64 ? kF64 : (p->acc == RV_ACC_NATIVE ? kF32Native : kF32Acc64);
   int U = 1;
-  p->kernel = pick_kernel(mode, p->C, vec, &U);
+  p->kernel = pick_kernel(mode, p->C, vec, push, &U);
   DeviceGuard g(p->device);
   RV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ, p->kernel, kThreads, 0));
   if (p->occ < 1) p->occ = 1;
   const int64_t tile_vecs = (int64_t)kThreads * U;
+  const int64_t unit_vecs = kUnitBytes / (N * es);
 
   free_lanes(p);
   p->lanes.resize(p->n_lanes);
   std::vector<int> loc = p->local;
   std::sort(loc.begin(), loc.end());
+  std::vector<int64_t> cursor(p->C, 0);  // push: staging cursor per owner, across lanes
   int64_t all_elems = 0;
   for (int l = 0; l < p->n_lanes; ++l) {
     rv_plan::Lane &lane = p->lanes[l];
     std::vector<Seg> segs;
     std::vector<int64_t> prefix(1, 0);
-    for (int r = l; r < p->R; r += p->n_lanes) {
-      lane.rings.push_back(r);
-      const int64_t base = p->rlen[r] / p->C, rem = p->rlen[r] % p->C;
-      int64_t lo = p->rstart[r];
-      std::vector<std::pair<int64_t, int64_t>> bounds(p->C);
-      for (int k = 0; k < p->C; ++k) {  // multiring.py:134-144
-        const int64_t n = base + (k < rem ? 1 : 0);
-        bounds[k] = {lo, lo + n};
-        lo += n;
-      }
-      for (int k : loc) {
-        Seg s;
-        s.lo = bounds[k].first;
-        s.hi = bounds[k].second;
-        s.k = k;
-        s.ring = r;
-        if (s.hi <= s.lo) continue;
-        int64_t blo = s.lo + ((N - (s.lo + a0) % N) % N);
-        int64_t bhi = s.hi - ((s.hi + a0) % N);
-        if (bhi <= blo) {
-          blo = bhi = s.hi;  // no aligned vector: all edge elements (< 2N)
+    for (int r = l; r < p->R; r += p->n_lanes) lane.rings.push_back(r);
+    if (!push) {
+      for (int r : lane.rings) {
+        const auto bounds = ring_chunks(p, r);
+        for (int k : loc) {
+          Seg s{};
+          s.lo = bounds[k].first;
+          s.hi = bounds[k].second;
+          s.k = k;
+          s.ring = r;
+          if (s.hi <= s.lo) continue;
+          set_body(s, N, a0);
+          const int64_t nvec = (s.body_hi - s.body_lo) / N;
+          segs.push_back(s);
+          prefix.push_back(prefix.back() + std::max<int64_t>(1, (nvec + tile_vecs - 1) / tile_vecs));
+          lane.elems += s.hi - s.lo;
         }
-        s.body_lo = blo;
-        s.body_hi = bhi;
-        const int64_t nvec = (bhi - blo) / N;
-        const int64_t tiles = std::max<int64_t>(1, (nvec + tile_vecs - 1) / tile_vecs);
-        segs.push_back(s);
-        prefix.push_back(prefix.back() + tiles);
-        lane.elems += s.hi - s.lo;
       }
+      lane.nseg = (int)segs.size();
+      lane.n_tiles = prefix.back();
+      int rc = upload(lane, segs, prefix);
+      if (rc) return rc;
+    } else {
+      // every owner's chunks (owner-major): writers need the owners' layouts
+      lane.ounits.assign(p->C, 0);
+      lane.oseg_base.assign(p->C + 1, 0);
+      for (int q = 0; q < p->C; ++q) {
+        lane.oseg_base[q] = (int)segs.size();
+        int64_t u = 0;
+        for (int r : lane.rings) {
+          const auto bounds = ring_chunks(p, r);
+          Seg s{};
+          s.lo = bounds[q].first;
+          s.hi = bounds[q].second;
+          s.k = q;
+          s.ring = r;
+          if (s.hi <= s.lo) continue;
+          set_body(s, N, a0);
+          // staging index of element i is stage_off + (i - lo); keep it
+          // vector-aligned exactly where the source is
+          const int64_t c0 = (cursor[q] + N - 1) / N * N;
+          s.stage_off = c0 + ((s.lo + a0) % N);
+          cursor[q] = s.stage_off + (s.hi - s.lo);
+          s.unit0 = u;
+          const int64_t nvec = (s.body_hi - s.body_lo) / N;
+          u += std::max<int64_t>(1, (nvec + unit_vecs - 1) / unit_vecs);
+          segs.push_back(s);
+          if (q == p->rank) lane.elems += s.hi - s.lo;
+        }
+        lane.ounits[q] = u;
+        if (u > p->units_max) return set_err(RV_E_ARG, "push unit bound exceeded (%lld > %lld)",
+                                             (long long)u, (long long)p->units_max);
+      }
+      lane.oseg_base[p->C] = (int)segs.size();
+      lane.unit_vecs = unit_vecs;
+      lane.scatter_umax = 0;
+      for (int q = 0; q < p->C; ++q)
+        if (q != p->rank) lane.scatter_umax = std::max(lane.scatter_umax, lane.ounits[q]);
+      lane.nseg = (int)segs.size();
+      lane.n_tiles = (int64_t)(p->C - 1) * lane.scatter_umax + lane.ounits[p->rank];
+      int rc = upload(lane, segs, {});
+      if (rc) return rc;
     }
-    lane.nseg = (int)segs.size();
-    lane.n_tiles = prefix.back();
     all_elems += lane.elems;
-    if (lane.nseg > 0) {
-      RV_CUDA(cudaMalloc(&lane.segs, sizeof(Seg) * segs.size()));
-      RV_CUDA(cudaMalloc(&lane.prefix, sizeof(int64_t) * prefix.size()));
-      RV_CUDA(cudaMemcpy(lane.segs, segs.data(), sizeof(Seg) * segs.size(), cudaMemcpyHostToDevice));
-      RV_CUDA(cudaMemcpy(lane.prefix, prefix.data(), sizeof(int64_t) * prefix.size(), cudaMemcpyHostToDevice));
-    }
+  }
+  if (push) {
+    int64_t stride = 0;
+    for (int q = 0; q < p->C; ++q) stride = std::max(stride, cursor[q]);
+    stride = (stride + 15) / 16 * 16;
+    if (stride > p->stride_bound)
+      return set_err(RV_E_ARG, "push staging bound exceeded (%lld > %lld)", (long long)stride,
+                     (long long)p->stride_bound);
+    for (auto &lane : p->lanes) lane.stride = p->stride_bound;
   }
   // persistent grid: all lanes together fit in one wave (no lane can starve
   // another on this device while both wait on peers)
   const int64_t capacity = (int64_t)p->sm_count * p->occ;
-  int64_t used = 0;
   for (int l = 0; l < p->n_lanes; ++l) {
     rv_plan::Lane &lane = p->lanes[l];
     int64_t share = all_elems > 0 ? capacity * lane.elems / all_elems : 0;
     if (p->n_lanes == 1) share = capacity;
     share = std::max<int64_t>(1, std::min<int64_t>(share, std::max<int64_t>(1, lane.n_tiles)));
     lane.grid = (int)share;
-    used += share;
   }
-  (void)used;
   p->dirty = false;
   return RV_OK;
 }
@@ -557,10 +824,23 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
   cp.rank = p->rank;
   cp.n_ranks = p->n_ranks;
   cp.lane = l;
+  cp.me = p->local.empty() ? 0 : p->local[0];
   cp.pow2 = (p->C & (p->C - 1)) == 0;
   cp.inv_c = 1.0 / (double)p->C;
-  if (lane.nseg == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet
-  int grid = std::max(1, lane.grid);
+  if (p->use_push) {
+    for (int q = 0; q < p->C; ++q) {
+      cp.pflags[q] = reinterpret_cast<unsigned long long *>(p->peer_push[q]);
+      cp.stage[q] = p->peer_push[q] + p->pflag_bytes;
+      cp.ounits[q] = lane.ounits[q];
+    }
+    for (int q = 0; q <= p->C; ++q) cp.oseg_base[q] = lane.oseg_base[q];
+    cp.stride = lane.stride;
+    cp.units_max = p->units_max;
+    cp.scatter_umax = lane.scatter_umax;
+    cp.unit_vecs = lane.unit_vecs;
+  }
+  if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet
+  const int grid = std::max(1, lane.grid);
   p->kernel<<<grid, kThreads, 0, st>>>(cp);
   RV_CUDA(cudaGetLastError());
   return RV_OK;
@@ -705,6 +985,46 @@ int rv_plan_set_peers(rv_plan *p, int rank, int n_ranks, void *const *areas) {
   return RV_OK;
 }
 
+int rv_plan_set_protocol(rv_plan *p, int proto) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  if (proto != RV_PROTO_PULL && proto != RV_PROTO_PUSH) return set_err(RV_E_CONFIG, "unknown protocol %d", proto);
+  p->proto = proto;
+  p->dirty = true;
+  return RV_OK;
+}
+
+int rv_plan_push_area(rv_plan *p, void **area, size_t *bytes) {
+  if (!p || !area) return set_err(RV_E_ARG, "NULL argument");
+  if (p->push_area && p->push_lanes != p->n_lanes) {
+    DeviceGuard g(p->device);
+    cudaFree(p->push_area);
+    p->push_area = nullptr;
+  }
+  if (!p->push_area) {
+    push_bounds(p, &p->stride_bound, &p->units_max);
+    const size_t nflags = (size_t)std::max(1, p->n_lanes) * p->C * p->units_max;
+    p->pflag_bytes = (nflags * sizeof(unsigned long long) + 4095) / 4096 * 4096;
+    p->push_bytes = p->pflag_bytes + (size_t)p->C * p->stride_bound * elem_size(p->dtype);
+    DeviceGuard g(p->device);
+    RV_CUDA(cudaMalloc(&p->push_area, p->push_bytes));
+    RV_CUDA(cudaMemset(p->push_area, 0, p->pflag_bytes));
+    RV_CUDA(cudaDeviceSynchronize());
+    p->push_lanes = p->n_lanes;
+    p->dirty = true;
+  }
+  *area = p->push_area;
+  if (bytes) *bytes = p->push_bytes;
+  return RV_OK;
+}
+
+int rv_plan_set_push_peers(rv_plan *p, void *const *areas) {
+  if (!p || !areas) return set_err(RV_E_ARG, "NULL argument");
+  p->peer_push.assign(RV_MAX_RANKS, nullptr);
+  for (int r = 0; r < p->n_ranks; ++r) p->peer_push[r] = static_cast<char *>(areas[r]);
+  p->dirty = true;
+  return RV_OK;
+}
+
 int rv_plan_set_timeout(rv_plan *p, double seconds) {
   if (!p || !(seconds > 0)) return set_err(RV_E_ARG, "bad timeout");
   p->timeout_ns = (unsigned long long)(seconds * 1e9);
@@ -776,11 +1096,11 @@ int rv_plan_status(rv_plan *p, char *diag, size_t diag_len) {
   std::string rings;
   if (lane < p->lanes.size())
     for (int r : p->lanes[lane].rings) rings += (rings.empty() ? "" : "|") + std::to_string(r);
+  const char *ph = phase == 0 ? "arrive" : phase == 1 ? "depart" : "unit";
   if (diag && diag_len)
-    snprintf(diag, diag_len, "waiting on: (ring=%s, phase=%s, rank=%u)", rings.empty() ? "?" : rings.c_str(),
-             phase == 0 ? "arrive" : "depart", peer);
-  return set_err(RV_E_TIMEOUT, "peer rank %u never reached the %s barrier (lane %u)", peer,
-                 phase == 0 ? "arrive" : "depart", lane);
+    snprintf(diag, diag_len, "waiting on: (ring=%s, phase=%s, rank=%u)", rings.empty() ? "?" : rings.c_str(), ph,
+             peer);
+  return set_err(RV_E_TIMEOUT, "peer rank %u never reached the %s barrier (lane %u)", peer, ph, lane);
 }
 
 int rv_plan_reset_status(rv_plan *p) {
@@ -796,6 +1116,7 @@ int rv_plan_destroy(rv_plan *p) {
   {
     DeviceGuard g(p->device);
     free_lanes(p);
+    if (p->push_area) cudaFree(p->push_area);
     if (p->flags) cudaFree(p->flags);
     if (p->states) cudaFree(p->states);
     if (p->status) cudaFree(p->status);

@@ -71,7 +71,7 @@ class DistRingGroup:
 
     def __init__(self, schedule=None, src=None, dst=None, *, starts: Sequence[int] | None = None,
                  lens: Sequence[int] | None = None, cluster_id: int | None = None, acc: str = "f64",
-                 lanes: int = 1, group=None, timeout_s: float | None = None):
+                 lanes: int = 1, group=None, timeout_s: float | None = None, protocol: str = "pull"):
         import torch.distributed as dist
 
         if src is None:
@@ -110,6 +110,8 @@ class DistRingGroup:
             self.plan.set_lanes(lanes)
         if timeout_s is not None:
             self.plan.set_timeout(timeout_s)
+        self.protocol = protocol
+        self.plan.set_protocol(protocol)
         flag_ptr, _ = self.plan.flag_area()
         mine = {
             "cid": cid,
@@ -117,23 +119,34 @@ class DistRingGroup:
             "dst": _export(dst.data_ptr()),
             "flags": _export(flag_ptr),
         }
+        push_ptr = 0
+        if protocol == "push":
+            push_ptr, _ = self.plan.push_area()
+            mine["push"] = _export(push_ptr)
         everyone, order, self.position = rendezvous(mine, group)
         self._imported: list[int] = []
         areas = [0] * self.world
+        push_areas = [0] * self.world
         for pos, r in enumerate(order):
             e = everyone[r]
             if r == self.rank:
                 self.plan.bind(pos, src.data_ptr(), dst.data_ptr())
                 areas[pos] = flag_ptr
+                push_areas[pos] = push_ptr
                 continue
             s = _import(self.device, *e["src"])
             d = s if e["dst"] == e["src"] else _import(self.device, *e["dst"])
             f = _import(self.device, *e["flags"])
             self._imported += [s, f] + ([d] if d != s else [])
+            if protocol == "push":
+                push_areas[pos] = _import(self.device, *e["push"])
+                self._imported.append(push_areas[pos])
             self.plan.bind(pos, s, d)
             areas[pos] = f
         self.plan.set_local([self.position])
         self.plan.set_peers(self.position, self.world, areas)
+        if protocol == "push":
+            self.plan.set_push_peers(push_areas)
         dist.barrier(group=group)
 
     def average(self, streams=None) -> None:

@@ -20,6 +20,7 @@ from . import _native as N
 from .errors import ConfigError, LayoutError
 
 ACC_MODES = {"f64": N.RV_ACC_F64, "native": N.RV_ACC_NATIVE}
+PROTOCOLS = {"pull": N.RV_PROTO_PULL, "push": N.RV_PROTO_PUSH}
 
 
 def _dtype_code(dtype) -> int:
@@ -72,6 +73,20 @@ class DevicePlan:
 
     def set_lanes(self, n: int) -> None:
         N.check(self.lib.rv_plan_set_lanes(self._h, int(n)), "rv_plan_set_lanes")
+
+    def set_protocol(self, proto: str) -> None:
+        if proto not in PROTOCOLS:
+            raise ConfigError(f"unknown protocol {proto!r} (use 'pull' or 'push')")
+        N.check(self.lib.rv_plan_set_protocol(self._h, PROTOCOLS[proto]), "rv_plan_set_protocol")
+
+    def push_area(self) -> tuple[int, int]:
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        N.check(self.lib.rv_plan_push_area(self._h, ctypes.byref(p), ctypes.byref(n)), "rv_plan_push_area")
+        return int(p.value or 0), int(n.value)
+
+    def set_push_peers(self, areas: Sequence[int]) -> None:
+        N.check(self.lib.rv_plan_set_push_peers(self._h, N.ptr_array(areas)), "rv_plan_set_push_peers")
 
     def set_timeout(self, seconds: float) -> None:
         N.check(self.lib.rv_plan_set_timeout(self._h, float(seconds)), "rv_plan_set_timeout")

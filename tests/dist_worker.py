@@ -41,14 +41,15 @@ def main():
         total = sum(lens)
         starts = list(np.cumsum([0] + lens[:-1]))
         big = total > 10_000_000
-        variants = [("f64", torch.float32, 1, False, False)] if big else [
+        base = [("f64", torch.float32, 1, False, False)] if big else [
             ("f64", torch.float32, 1, False, False),
             ("native", torch.float32, 1, True, False),
             ("f64", torch.float64, 1, False, True),
             ("f64", torch.float32, len(lens), False, False),
             ("f64", torch.float32, 1, False, True),
         ]
-        for acc, dt, lanes, reverse_ids, src_ne_dst in variants:
+        variants = [v + (proto,) for proto in ("pull", "push") for v in base]
+        for acc, dt, lanes, reverse_ids, src_ne_dst, proto in variants:
             npdt = np.float32 if dt == torch.float32 else np.float64
             xs = [np.random.Generator(np.random.Philox(key=1000 * ci + m)).normal(0, 1, total).astype(npdt)
                   for m in range(world)]
@@ -61,7 +62,8 @@ def main():
             x = buf[off:off + total]
             x.copy_(torch.from_numpy(xs[rank]))
             dst = torch.full((total,), float("nan"), dtype=dt, device=f"cuda:{local}") if src_ne_dst else None
-            g = DistRingGroup(src=x, dst=dst, starts=starts, lens=lens, cluster_id=cid, acc=acc, lanes=lanes)
+            g = DistRingGroup(src=x, dst=dst, starts=starts, lens=lens, cluster_id=cid, acc=acc, lanes=lanes,
+                              protocol=proto)
             streams = [torch.cuda.Stream() for _ in range(lanes)]
             for s in streams:
                 s.wait_stream(torch.cuda.current_stream())
@@ -71,7 +73,7 @@ def main():
             got = (dst if dst is not None else x).cpu().numpy()
             if not np.array_equal(bits(got), bits(want)):
                 bad = int(np.sum(bits(got) != bits(want)))
-                print(f"rank {rank} case {ci} {acc} {dt} lanes={lanes} rev={reverse_ids}: {bad} mismatches",
+                print(f"rank {rank} case {ci} {proto} {acc} {dt} lanes={lanes} rev={reverse_ids}: {bad} mismatches",
                       flush=True)
                 failures += 1
             if not big and not src_ne_dst and lanes == 1:
@@ -83,7 +85,22 @@ def main():
                     torch.cuda.synchronize()
                 g.check()
                 if not np.array_equal(bits(h_out.numpy()), bits(want)):
-                    print(f"rank {rank} case {ci} host path mismatch", flush=True)
+                    print(f"rank {rank} case {ci} {proto} host path mismatch", flush=True)
+                    failures += 1
+            if not big and not src_ne_dst and lanes == 1 and acc == "f64" and dt == torch.float32:
+                # three cycles back to back, no host sync in between (epoch handling)
+                x.copy_(torch.from_numpy(xs[rank]))
+                torch.cuda.synchronize()
+                dist.barrier()
+                for _ in range(3):
+                    g.average()
+                torch.cuda.synchronize()
+                g.check()
+                cur = vals
+                for _ in range(3):
+                    cur = [v.astype(npdt) for v in ring_oracle.ring_mean(starts, lens, cur, acc=acc)]
+                if not np.array_equal(bits(x.cpu().numpy()), bits(cur[order.index(rank)])):
+                    print(f"rank {rank} case {ci} {proto} back-to-back mismatch", flush=True)
                     failures += 1
             dist.barrier()
             g.close()
