@@ -652,7 +652,7 @@ void push_bounds(const rv_plan *p, int64_t *stride_bound, int64_t *units_max) {
     umax = std::max(umax, u);
   }
   for (int r = 0; r < p->R; ++r) stride += (p->rlen[r] + p->C - 1) / p->C + 2 * nmax;
-  *stride_bound = stride;
+  *stride_bound = (stride + 63) / 64 * 64;  // writer slots stay 256-byte aligned
   *units_max = umax;
 }
 

@@ -29,7 +29,7 @@ import numpy as np
 
 from .errors import ConfigError, LayoutError, RavnestError, StallError
 from .plan import LocalRingGroup
-from .schedule import RingStats, ring_arrays, schedule_stats
+from .schedule import RingStats, chunk_bounds, ring_arrays, schedule_stats
 
 _GROUPS: "collections.OrderedDict[tuple, LocalRingGroup]" = collections.OrderedDict()
 _MAX_GROUPS = 8
@@ -136,23 +136,45 @@ def apply_ring_mean(schedule, cluster_params: dict, acc: str = "f64") -> dict:
     return work
 
 
-def _fifo_progress(schedule, n_clusters: int, budget: int):
-    """Emulate the ideal network's FIFO delivery order (simnet.py:99-112 with
-    every event at t=0) for ``budget`` events; returns per-ring expected
-    rounds, as AllReduceController._expected (multiring.py:176)."""
+def _ideal_network_progress(schedule, n_clusters: int, budget: int,
+                            node_of: Callable[[int, int], str] = default_node_name):
+    """Replay, without data, how far the reference's cycle gets on its ideal
+    network within ``budget`` events: every link has bandwidth 1e18 B/s and
+    zero latency (multiring.py:278-285), so a chunk of n float64 values is
+    delivered n*8/1e18 s after its link frees up (simnet.py:165-187), ties by
+    send order (simnet.py:70-113).  Returns AllReduceController._expected."""
+    import heapq
+
     expected = {r.ring_id: [0] * n_clusters for r in schedule.rings}
     last = 2 * (n_clusters - 1)
-    queue = collections.deque()
+    rings = {r.ring_id: r for r in schedule.rings}
+    bounds = {r.ring_id: chunk_bounds(r.start, r.length, n_clusters) for r in schedule.rings}
+    busy: dict = {}
+    heap: list = []
+    seq = 0
+
+    def send(rid, pos, rnd, chunk, now):
+        nonlocal seq
+        ring = rings[rid]
+        link = (node_of(*ring.members[pos]), node_of(*ring.members[(pos + 1) % n_clusters]))
+        lo, hi = bounds[rid][chunk]
+        start = max(now, busy.get(link, 0.0))
+        done = start + (hi - lo) * 8 / 1e18
+        busy[link] = done
+        heapq.heappush(heap, (done + 0.0, seq, (rid, (pos + 1) % n_clusters, rnd, chunk)))
+        seq += 1
+
     for r in schedule.rings:
         for pos in range(n_clusters):
-            queue.append((r.ring_id, (pos + 1) % n_clusters, 0))
-    done = 0
-    while queue and done < budget:
-        rid, to_pos, rnd = queue.popleft()
+            send(r.ring_id, pos, 0, pos % n_clusters, 0.0)
+    now, done_events = 0.0, 0
+    while heap and done_events < budget:
+        t, _, (rid, to_pos, rnd, chunk) = heapq.heappop(heap)
+        now = max(now, t)
         expected[rid][to_pos] = rnd + 1
-        done += 1
+        done_events += 1
         if rnd + 1 < last:
-            queue.append((rid, (to_pos + 1) % n_clusters, rnd + 1))
+            send(rid, to_pos, rnd + 1, chunk, now)
     return expected
 
 
@@ -182,7 +204,7 @@ def run_allreduce(schedule, cluster_params: dict, network=None,
     c = len(cids)
     needed = sum(2 * (c - 1) * c for _ in schedule.rings)
     if max_events is not None and max_events < needed:
-        expected = _fifo_progress(schedule, c, max_events)
+        expected = _ideal_network_progress(schedule, c, max_events, node_of)
         raise StallError(
             f"event budget of {max_events} exhausted\n"
             + "all-reduce incomplete: " + _stall_text(schedule, expected, c)

@@ -10,6 +10,19 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+REFERENCE_SRC = "/root/reference/pkg/src"  # dev container only; absent on GPU boxes
+
+
+def import_reference(module: str = "ravnest"):
+    """The unmodified reference (CPU checks in the dev container), or skip."""
+    if not os.path.isdir(REFERENCE_SRC):
+        pytest.skip("reference not present here")
+    sys.dont_write_bytecode = True
+    if REFERENCE_SRC not in sys.path:
+        sys.path.append(REFERENCE_SRC)
+    import importlib
+
+    return importlib.import_module(module)
 
 
 def pytest_configure(config):
