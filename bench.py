@@ -247,14 +247,27 @@ def warm_under_load(step, warmup: int, seconds: float = 0.6, lockstep: bool = Fa
     torch.cuda.synchronize()
 
 
-def time_steps(fn, stream, steps: int):
-    """Per-step CUDA-event durations (ms) on `stream`."""
+def stale_live(snap, key: int, tau: int, eta: float = 1e-3):
+    """live = snap - eta * sum_{j=1..tau} g_j, g_j ~ N(0,1) seeded per (cluster, j)
+    (the tau updates that landed after the snapshot)."""
     import torch
 
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    for a, b in evs:
+    live = snap.clone()
+    for j in range(1, tau + 1):
+        g = torch.Generator(device=snap.device).manual_seed(SEED * 7919 + key * 31 + j)
+        live.sub_(torch.randn(snap.numel(), device=snap.device, generator=g), alpha=eta)
+    return live
+
+
+def time_steps(fn, stream, steps: int):
+    """Per-step CUDA events on `stream`: (start, after-averaging, end).  The
+    first interval is the averaging launch(es) alone -- the roofline basis."""
+    import torch
+
+    evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(steps)]
+    for a, m, b in evs:
         a.record(stream)
-        fn()
+        fn(m)
         b.record(stream)
     return evs
 
@@ -263,6 +276,7 @@ def run_single(args):
     """N = 1: C clusters co-resident on cuda:0."""
     import torch
 
+    from paper_2401_01728_b200.blend import blend_
     from paper_2401_01728_b200.plan import LocalRingGroup
 
     lens = WORKLOADS[args.workload]
@@ -271,12 +285,16 @@ def run_single(args):
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
     xs = [synth(total, m, dev) for m in range(c)]
+    lives = means = None
+    if args.blend:
+        lives = [stale_live(x, m, args.tau) for m, x in enumerate(xs)]
+        means = [torch.empty_like(x) for x in xs]
     g = LocalRingGroup(ring_starts(lens), lens, total, [0] * c, torch.float32, acc=args.acc, lanes=args.lanes)
-    g.bind_tensors(xs)
+    g.bind_tensors(xs, means)
     stream = torch.cuda.current_stream()
     lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
 
-    def step():
+    def step(mid=None):
         if lane_streams:
             for s in lane_streams:
                 s.wait_stream(stream)
@@ -285,6 +303,11 @@ def run_single(args):
                 stream.wait_stream(s)
         else:
             g.run({0: [stream]})
+        if mid is not None:
+            mid.record(stream)
+        if args.blend:
+            for m in range(c):
+                blend_(lives[m], xs[m], means[m], stream)
 
     clocks = ClockSampler(0)
     clocks.start()
@@ -299,9 +322,8 @@ def run_single(args):
     clk = clocks.stop()
     g.check()
     total_ms = t_start.elapsed_time(t_end)
-    per = [a.elapsed_time(b) for a, b in evs]
     ms = total_ms / args.steps
-    kernel_ms = statistics.mean(per)
+    kernel_ms = statistics.mean(a.elapsed_time(m) for a, m, _ in evs)
 
     # e2e: host (pinned) buffers -> device -> average -> host, via the C ABI
     hsrc = [x.cpu().pin_memory() for x in xs]
@@ -352,11 +374,13 @@ def run_single(args):
         "metric": METRIC, "value": round(bw, 3), "unit": "GB/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "ms_per_round": round(ms / (2 * (c - 1)), 5),
+        "avg_kernel_ms": round(kernel_ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
         "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
         "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                    "placement": "co-resident on cuda:0", "lanes": args.lanes, "parallelism": "replicas only",
+                   "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
                    "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4), "traffic": None,
@@ -369,7 +393,7 @@ def run_single(args):
                 "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": c * total * 4, "d2h_bytes_per_step": c * total * 4,
                 "path": "rv_allreduce_mean_host (pinned host fp32, per-ring lanes)"},
-        "gpu_launches": args.steps * args.lanes,
+        "gpu_launches": args.steps * (args.lanes + (c if args.blend else 0)),
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
@@ -379,6 +403,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
 
+    from paper_2401_01728_b200.blend import blend_
     from paper_2401_01728_b200.dist import DistRingGroup
 
     lens = WORKLOADS[args.workload]
@@ -386,12 +411,18 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     dev = torch.device(f"cuda:{local_rank}")
     torch.cuda.set_device(dev)
     x = synth(total, rank, dev)
-    grp = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes,
+    live = mean = None
+    if args.blend:
+        # config 4: average a snapshot x into `mean`, then blend the tau
+        # pending updates of `live` onto it (live <- mean + (live - snap))
+        live = stale_live(x, rank, args.tau)
+        mean = torch.empty_like(x)
+    grp = DistRingGroup(src=x, dst=mean, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes,
                         protocol=args.protocol)
     stream = torch.cuda.current_stream()
     lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
 
-    def step():
+    def step(mid=None):
         if lane_streams:
             for s in lane_streams:
                 s.wait_stream(stream)
@@ -400,6 +431,10 @@ def run_multi(args, rank: int, world: int, local_rank: int):
                 stream.wait_stream(s)
         else:
             grp.average([stream])
+        if mid is not None:
+            mid.record(stream)
+        if args.blend:
+            blend_(live, x, mean, stream)
 
     clocks = ClockSampler(local_rank) if rank == 0 else None
     if clocks:
@@ -418,7 +453,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     clk = clocks.stop() if clocks else None
     grp.check()
     ms_local = a.elapsed_time(b) / args.steps
-    kern_local = statistics.mean(ea.elapsed_time(eb) for ea, eb in evs)
+    kern_local = statistics.mean(ea.elapsed_time(em) for ea, em, _ in evs)
     t = torch.tensor([ms_local, kern_local], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # gloo, outside the timed region
     ms, kernel_ms = float(t[0]), float(t[1])
@@ -467,12 +502,14 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "metric": METRIC, "value": round(bw * world, 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "ms_per_round": round(ms / (2 * (c - 1)), 5),
+            "avg_kernel_ms": round(kernel_ms, 4),
             "bus_gbps_per_gpu": round(bw, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
             "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
             "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                        "placement": "one cluster per GPU", "lanes": args.lanes, "protocol": args.protocol,
+                       "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
                        "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
                        "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
@@ -483,7 +520,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
                     "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": world * total * 4, "d2h_bytes_per_step": world * total * 4,
                     "path": "rv_allreduce_mean_host (pinned host fp32, per-ring lanes)"},
-            "gpu_launches": args.steps * args.lanes * world,
+            "gpu_launches": args.steps * (args.lanes + (1 if args.blend else 0)) * world,
             "clocks": clk,
         }
         if nccl:
@@ -539,6 +576,8 @@ def main():
     ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")
     ap.add_argument("--cpu-sample-params", type=int, default=8_000_000)
     ap.add_argument("--nccl", type=int, default=1)
+    ap.add_argument("--blend", type=int, default=0, help="config 4: snapshot average + delayed-update blend")
+    ap.add_argument("--tau", type=int, default=4)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

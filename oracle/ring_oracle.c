@@ -18,7 +18,7 @@
  *                   (indices mod C, x_m = m-th smallest cluster id).
  *   working dtype   float64 (multiring.py:309 widens every input).
  *
- * Build: oracle/Makefile -> oracle/_build/libring_oracle.so (gcc, -O2,
+ * Build: oracle/Makefile -> oracle/_build/libring_oracle.so (gcc, -O3,
  * -ffp-contract=off: every add and the divide stay single IEEE ops).
  */
 #include <pthread.h>
@@ -45,43 +45,68 @@ typedef struct {
   int64_t begin, end;   /* this worker's slice of the concatenated chunks */
 } rvo_job;
 
+/* Fold [lo, hi) of a chunk whose ring order starts at member k.  Blocked so
+ * every inner loop is a unit-stride loop the compiler vectorises; the
+ * per-element operation order is unchanged (x_k first, then x_{k+1}, ...). */
+#define RVO_BLK 512
 static void run_range(const rvo_job *j, const rvo_seg *s, int64_t lo, int64_t hi) {
   const int c = j->c;
+  int order[64];
+  for (int t = 0; t < c; ++t) order[t] = (s->k + t) % c;
   if (j->mode == RVO_MODE_F64) {
     const double *const *x = (const double *const *)j->in;
     double *const *y = (double *const *)j->out;
     const double div = (double)c;
-    for (int64_t i = lo; i < hi; ++i) {
-      double acc = x[s->k][i];
-      for (int t = 1; t < c; ++t) acc = acc + x[(s->k + t) % c][i];
-      acc = acc / div;
-      for (int m = 0; m < c; ++m) y[m][i] = acc;
+    double acc[RVO_BLK];
+    for (int64_t b0 = lo; b0 < hi; b0 += RVO_BLK) {
+      const int n = (int)(hi - b0 < RVO_BLK ? hi - b0 : RVO_BLK);
+      const double *x0 = x[order[0]] + b0;
+      for (int i = 0; i < n; ++i) acc[i] = x0[i];
+      for (int t = 1; t < c; ++t) {
+        const double *xt = x[order[t]] + b0;
+        for (int i = 0; i < n; ++i) acc[i] = acc[i] + xt[i];
+      }
+      for (int i = 0; i < n; ++i) acc[i] = acc[i] / div;
+      for (int m = 0; m < c; ++m) memcpy(y[m] + b0, acc, sizeof(double) * (size_t)n);
     }
   } else if (j->mode == RVO_MODE_F32_ACC64) {
     const float *const *x = (const float *const *)j->in;
     double *const *y = (double *const *)j->out;
     float *const *y32 = j->out32;
     const double div = (double)c;
-    for (int64_t i = lo; i < hi; ++i) {
-      double acc = (double)x[s->k][i];
-      for (int t = 1; t < c; ++t) acc = acc + (double)x[(s->k + t) % c][i];
-      acc = acc / div;
+    double acc[RVO_BLK];
+    float acc32[RVO_BLK];
+    for (int64_t b0 = lo; b0 < hi; b0 += RVO_BLK) {
+      const int n = (int)(hi - b0 < RVO_BLK ? hi - b0 : RVO_BLK);
+      const float *x0 = x[order[0]] + b0;
+      for (int i = 0; i < n; ++i) acc[i] = (double)x0[i];
+      for (int t = 1; t < c; ++t) {
+        const float *xt = x[order[t]] + b0;
+        for (int i = 0; i < n; ++i) acc[i] = acc[i] + (double)xt[i];
+      }
+      for (int i = 0; i < n; ++i) acc[i] = acc[i] / div;
       if (y)
-        for (int m = 0; m < c; ++m) y[m][i] = acc;
+        for (int m = 0; m < c; ++m) memcpy(y[m] + b0, acc, sizeof(double) * (size_t)n);
       if (y32) {
-        const float f = (float)acc;
-        for (int m = 0; m < c; ++m) y32[m][i] = f;
+        for (int i = 0; i < n; ++i) acc32[i] = (float)acc[i];
+        for (int m = 0; m < c; ++m) memcpy(y32[m] + b0, acc32, sizeof(float) * (size_t)n);
       }
     }
   } else {
     const float *const *x = (const float *const *)j->in;
     float *const *y = (float *const *)j->out;
     const float div = (float)c;
-    for (int64_t i = lo; i < hi; ++i) {
-      float acc = x[s->k][i];
-      for (int t = 1; t < c; ++t) acc = acc + x[(s->k + t) % c][i];
-      acc = acc / div;
-      for (int m = 0; m < c; ++m) y[m][i] = acc;
+    float acc[RVO_BLK];
+    for (int64_t b0 = lo; b0 < hi; b0 += RVO_BLK) {
+      const int n = (int)(hi - b0 < RVO_BLK ? hi - b0 : RVO_BLK);
+      const float *x0 = x[order[0]] + b0;
+      for (int i = 0; i < n; ++i) acc[i] = x0[i];
+      for (int t = 1; t < c; ++t) {
+        const float *xt = x[order[t]] + b0;
+        for (int i = 0; i < n; ++i) acc[i] = acc[i] + xt[i];
+      }
+      for (int i = 0; i < n; ++i) acc[i] = acc[i] / div;
+      for (int m = 0; m < c; ++m) memcpy(y[m] + b0, acc, sizeof(float) * (size_t)n);
     }
   }
 }
@@ -104,7 +129,7 @@ static void *worker(void *arg) {
 int rvo_ring_mean(int mode, int c, int n_rings, const int64_t *ring_start,
                   const int64_t *ring_len, const void *const *in, void *const *out,
                   float *const *out32, int n_threads) {
-  if (c < 1 || n_rings < 0 || mode < 0 || mode > 2) return -1;
+  if (c < 1 || c > 64 || n_rings < 0 || mode < 0 || mode > 2) return -1;
   if (c == 1) return 0; /* C == 1: nothing to average (orchestrator.py:325,328) */
   rvo_seg *segs = (rvo_seg *)malloc(sizeof(rvo_seg) * (size_t)(n_rings * c + 1));
   if (!segs) return -1;
