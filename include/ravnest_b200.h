@@ -114,6 +114,13 @@ int rv_plan_set_push_peers(rv_plan *plan, void *const *areas);
 
 int rv_plan_set_timeout(rv_plan *plan, double seconds);
 
+/* Phase tracing (off by default): per lane, the device globaltimer (ns) of
+ * [earliest block start, last block ready for data (pull: arrive barrier
+ * passed), last block done with data, depart barrier completed] of the most
+ * recent launch.  rv_plan_read_trace synchronises the device. */
+int rv_plan_set_trace(rv_plan *plan, int enable);
+int rv_plan_read_trace(rv_plan *plan, int lane, uint64_t *out4);
+
 /* One averaging cycle, asynchronous on the given CUDA streams (NULL/0 ->
  * the legacy default stream).  Replaces apply_ring_mean / run_allreduce /
  * AllReduceController.kickoff..done (multiring.py:180-232, 254-333). */

@@ -74,7 +74,8 @@ struct DeviceGuard {
 
 constexpr int kThreads = 256;
 constexpr unsigned kStatusTimeout = 1u;
-constexpr int64_t kUnitBytes = 256 * 1024;  // push protocol: bytes per flagged unit
+constexpr int64_t kUnitBytes = 256 * 1024;    // push protocol: largest flagged unit
+constexpr int64_t kMinUnitBytes = 16 * 1024;  // push protocol: smallest flagged unit
 
 struct Seg {
   int64_t lo, hi;            // chunk [lo, hi) in elements
@@ -103,6 +104,7 @@ struct CycleParams {
   unsigned long long *my_flags;
   LaneState *state;
   unsigned int *status;        // [0] code, [1] diag
+  unsigned long long *trace;   // optional: [start, ready, work done, departed] (globaltimer ns)
   int64_t n_tiles;             // pull
   int64_t stride;              // push: staging elements per writer slot
   int64_t units_max;           // push: unit-flag slots per (lane, writer)
@@ -176,18 +178,30 @@ __device__ void post_peers(const CycleParams &p, int phase, unsigned long long e
   }
 }
 
+// Optional phase trace (thread 0 of each block): earliest start, latest
+// "ready for data" (pull: arrive barrier passed), latest end of data work,
+// and the moment the depart barrier completed.
+__device__ __forceinline__ void trace_min(const CycleParams &p, int slot) {
+  if (p.trace) atomicMin(p.trace + slot, globaltimer());
+}
+__device__ __forceinline__ void trace_max(const CycleParams &p, int slot) {
+  if (p.trace) atomicMax(p.trace + slot, globaltimer());
+}
+
 // Exit barrier: the last block of this launch tells every peer that all of
 // this device's stores (local and remote) are done, then waits for theirs,
 // so nobody resumes training on a buffer a peer is still writing.
 __device__ void depart(const CycleParams &p, unsigned long long epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    trace_max(p, 2);
     __threadfence_system();
     const unsigned prev = atomicAdd(&p.state->done, 1u);
     if (prev == gridDim.x - 1) {
       __threadfence_system();
       post_peers(p, 1, epoch);
       if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
+      trace_max(p, 3);
       p.state->done = 0u;
       *(volatile unsigned long long *)&p.state->epoch = epoch;
       __threadfence();
@@ -304,6 +318,7 @@ ring_cycle_kernel(const __grid_constant__ CycleParams p) {
   __shared__ int s_go;
   unsigned long long epoch = 0;
 
+  if (threadIdx.x == 0) trace_min(p, 0);
   if (p.n_ranks > 1) {
     if (threadIdx.x == 0) {
       epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
@@ -316,6 +331,7 @@ ring_cycle_kernel(const __grid_constant__ CycleParams p) {
         }
         go = wait_peers(p, 0, epoch);
       }
+      trace_max(p, 1);
       s_go = go;
     }
     __syncthreads();
@@ -347,7 +363,12 @@ ring_cycle_kernel(const __grid_constant__ CycleParams p) {
       }
     }
   }
-  if (p.n_ranks > 1) depart(p, epoch);
+  if (p.n_ranks > 1) {
+    depart(p, epoch);
+  } else if (p.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) trace_max(p, 2);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -380,6 +401,8 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
   __shared__ int s_ok;
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) {
+    trace_min(p, 0);
+    trace_max(p, 1);
     s_epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
     s_ok = (*(volatile unsigned *)p.status == 0);
   }
@@ -576,6 +599,7 @@ struct rv_plan {
   int64_t stride_bound = 0, units_max = 0;
   int push_lanes = 0;
   std::vector<char *> peer_push;  // by rank
+  unsigned long long *trace = nullptr;  // lanes x 4, when tracing
   // built lane tables
   bool dirty = true;       // local positions / lanes / peers / protocol changed
   bool ptrs_dirty = true;  // buffers rebound: rebuild only if the alignment class changed
@@ -640,7 +664,7 @@ bool push_active(const rv_plan *p) { return p->proto == RV_PROTO_PUSH && p->n_ra
 // pointer is known): staging elements per writer slot, unit flags per lane.
 void push_bounds(const rv_plan *p, int64_t *stride_bound, int64_t *units_max) {
   const int es = elem_size(p->dtype);
-  const int64_t nmax = 16 / es, unit_elems = kUnitBytes / es;
+  const int64_t nmax = 16 / es, unit_elems = kMinUnitBytes / es;
   int64_t stride = nmax;
   int64_t umax = 1;
   for (int l = 0; l < p->n_lanes; ++l) {
@@ -703,7 +727,26 @@ int build_tables(rv_plan *p) {
   RV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ, p->kernel, kThreads, 0));
   if (p->occ < 1) p->occ = 1;
   const int64_t tile_vecs = (int64_t)kThreads * U;
-  const int64_t unit_vecs = kUnitBytes / (N * es);
+  // push: unit size adapts so that a cycle has >= ~2 work items per resident
+  // block (small shards stay parallel, large ones amortise the unit flags);
+  // it depends only on the schedule and the device model, so every rank
+  // derives the same layout
+  int64_t unit_vecs = kUnitBytes / (N * es);
+  if (push) {
+    int64_t owner_elems = 0;
+    for (int q = 0; q < p->C; ++q) {
+      int64_t e = 0;
+      for (int r = 0; r < p->R; ++r) {
+        const auto b = ring_chunks(p, r);
+        e += b[q].second - b[q].first;
+      }
+      owner_elems = std::max(owner_elems, e);
+    }
+    const int64_t items = std::max<int64_t>(1, 2LL * p->sm_count * p->occ);
+    const int64_t want = (owner_elems / N * (p->C - 1) + items - 1) / items;
+    const int64_t lo = kMinUnitBytes / (N * es), hi = kUnitBytes / (N * es);
+    unit_vecs = std::min(hi, std::max(lo, (want + kThreads - 1) / kThreads * kThreads));
+  }
 
   free_lanes(p);
   p->lanes.resize(p->n_lanes);
@@ -817,6 +860,11 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
   cp.my_flags = p->flags;
   cp.state = p->states + l;
   cp.status = p->status;
+  if (p->trace) {
+    cp.trace = p->trace + 4 * l;
+    RV_CUDA(cudaMemsetAsync(cp.trace, 0xff, sizeof(unsigned long long), st));
+    RV_CUDA(cudaMemsetAsync(cp.trace + 1, 0, 3 * sizeof(unsigned long long), st));
+  }
   cp.n_tiles = lane.n_tiles;
   cp.timeout_ns = p->timeout_ns;
   cp.C = p->C;
@@ -1025,6 +1073,30 @@ int rv_plan_set_push_peers(rv_plan *p, void *const *areas) {
   return RV_OK;
 }
 
+int rv_plan_set_trace(rv_plan *p, int enable) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  DeviceGuard g(p->device);
+  if (enable && !p->trace) {
+    const size_t n = 4 * (size_t)std::max(1, p->R);
+    RV_CUDA(cudaMalloc(&p->trace, n * sizeof(unsigned long long)));
+    RV_CUDA(cudaMemset(p->trace, 0, n * sizeof(unsigned long long)));
+  } else if (!enable && p->trace) {
+    cudaFree(p->trace);
+    p->trace = nullptr;
+  }
+  return RV_OK;
+}
+
+int rv_plan_read_trace(rv_plan *p, int lane, uint64_t *out4) {
+  if (!p || !out4) return set_err(RV_E_ARG, "NULL argument");
+  if (!p->trace) return set_err(RV_E_ARG, "tracing is off");
+  if (lane < 0 || lane >= std::max(1, p->R)) return set_err(RV_E_ARG, "bad lane %d", lane);
+  DeviceGuard g(p->device);
+  RV_CUDA(cudaDeviceSynchronize());
+  RV_CUDA(cudaMemcpy(out4, p->trace + 4 * lane, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return RV_OK;
+}
+
 int rv_plan_set_timeout(rv_plan *p, double seconds) {
   if (!p || !(seconds > 0)) return set_err(RV_E_ARG, "bad timeout");
   p->timeout_ns = (unsigned long long)(seconds * 1e9);
@@ -1117,6 +1189,7 @@ int rv_plan_destroy(rv_plan *p) {
     DeviceGuard g(p->device);
     free_lanes(p);
     if (p->push_area) cudaFree(p->push_area);
+    if (p->trace) cudaFree(p->trace);
     if (p->flags) cudaFree(p->flags);
     if (p->states) cudaFree(p->states);
     if (p->status) cudaFree(p->status);

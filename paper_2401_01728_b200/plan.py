@@ -88,6 +88,19 @@ class DevicePlan:
     def set_push_peers(self, areas: Sequence[int]) -> None:
         N.check(self.lib.rv_plan_set_push_peers(self._h, N.ptr_array(areas)), "rv_plan_set_push_peers")
 
+    def set_trace(self, enable: bool = True) -> None:
+        N.check(self.lib.rv_plan_set_trace(self._h, int(bool(enable))), "rv_plan_set_trace")
+
+    def read_trace(self, lane: int = 0) -> dict:
+        """Phase durations (us) of the last launch of `lane`: launch->ready
+        (pull: arrive barrier), ready->data done, data done->departed."""
+        out = (ctypes.c_uint64 * 4)()
+        N.check(self.lib.rv_plan_read_trace(self._h, int(lane), out), "rv_plan_read_trace")
+        t0, t1, t2, t3 = (int(v) for v in out)
+        t3 = t3 or t2
+        return {"ready_us": (t1 - t0) / 1e3, "data_us": (t2 - t1) / 1e3, "depart_us": (t3 - t2) / 1e3,
+                "total_us": (t3 - t0) / 1e3}
+
     def set_timeout(self, seconds: float) -> None:
         N.check(self.lib.rv_plan_set_timeout(self._h, float(seconds)), "rv_plan_set_timeout")
 

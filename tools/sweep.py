@@ -80,9 +80,25 @@ def main():
                     dist.barrier()
                     gms = timed(graph.replay, max(2, args.steps // args.graph_steps), stream) / args.graph_steps
                     g.check()
+                    # device-side phase trace of a few isolated cycles (max over ranks)
+                    g.plan.set_trace(True)
+                    acc = None
+                    for _ in range(5):
+                        dist.barrier()
+                        g.average([stream])
+                        torch.cuda.synchronize()
+                        tr = g.plan.read_trace(0)
+                        v = torch.tensor([tr["ready_us"], tr["data_us"], tr["depart_us"], tr["total_us"]],
+                                         dtype=torch.float64)
+                        acc = v if acc is None else acc + v
+                    g.plan.set_trace(False)
+                    acc /= 5
+                    dist.all_reduce(acc, op=dist.ReduceOp.MAX)
                     row[proto] = {"ms": round(ms, 5), "bus_gbps": round(busbw(total, world, ms * 1e-3), 2),
                                   "graph_ms": round(gms, 5),
-                                  "graph_bus_gbps": round(busbw(total, world, gms * 1e-3), 2)}
+                                  "graph_bus_gbps": round(busbw(total, world, gms * 1e-3), 2),
+                                  "phases_us": {k: round(float(x), 2) for k, x in
+                                                zip(("ready", "data", "depart", "total"), acc)}}
                     del graph
                     g.close()
                 views = [x[s:s + n] for s in starts]
