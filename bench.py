@@ -508,7 +508,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
             "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
             "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
-                       "placement": "one cluster per GPU", "lanes": args.lanes, "protocol": args.protocol,
+                       "placement": "one cluster per GPU", "lanes": args.lanes, "protocol": grp.protocol,
                        "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
                        "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
                        "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
@@ -572,7 +572,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert")
     ap.add_argument("--acc", choices=["f64", "native"], default="f64")
     ap.add_argument("--lanes", type=int, default=1)
-    ap.add_argument("--protocol", choices=["pull", "push"], default="pull")
+    ap.add_argument("--protocol", choices=["auto", "pull", "push"], default="auto")
     ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")
     ap.add_argument("--cpu-sample-params", type=int, default=8_000_000)
     ap.add_argument("--nccl", type=int, default=1)

@@ -311,8 +311,10 @@ __device__ __forceinline__ void fold_range(const CycleParams &p, const Seg &s, i
 // HBM or NVLink peer loads) and pushes the mean into every member.  Arrive
 // barrier first (peers' inputs final), depart barrier last.
 
-template <typename T, typename Acc, int CB, int VB, int U>
-__global__ void __launch_bounds__(kThreads)
+// MINB = 2 caps fp32 kernels at 128 registers (two 256-thread blocks per SM,
+// no spills); fp64 storage keeps its larger register set.
+template <typename T, typename Acc, int CB, int VB, int U, int MINB = (sizeof(T) == 4 ? 2 : 1)>
+__global__ void __launch_bounds__(kThreads, MINB)
 ring_cycle_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = VB / sizeof(T);
   __shared__ int s_go;
@@ -393,7 +395,7 @@ __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
 }
 
 template <typename T, typename Acc, int CB, int VB, int U>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 1)
 ring_push_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = VB / sizeof(T);
   constexpr int KC = (U * CB) < 16 ? (U * CB) : 16;  // vectors in flight per thread when copying
@@ -532,8 +534,30 @@ KernelFn pick_cb(int c, bool push) {
   return push ? ring_push_kernel<T, Acc, 16, VB, 1> : ring_cycle_kernel<T, Acc, 16, VB, 1>;
 }
 
+// Tuning variants of the f32 / f64-fold vector pull kernel (RAVNEST_B200_VARIANT,
+// experiments only): 1 = half the vectors per thread, >= 3 blocks/SM;
+// 2 = half, >= 4 blocks/SM; 3 = same vectors, >= 1 block/SM (no register cap).
+template <int CB, int U>
+KernelFn pick_variant(int v, int *u_out) {
+  constexpr int H = U > 1 ? U / 2 : 1;
+  switch (v) {
+    case 1: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 3>;
+    case 2: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 4>;
+    case 3: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 1>;
+    default: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 2>;
+  }
+}
+
 KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
   *u_out = c <= 2 ? 8 : c <= 4 ? 4 : c <= 8 ? 2 : 1;
+  const char *ve = getenv("RAVNEST_B200_VARIANT");
+  const int variant = ve ? atoi(ve) : 0;
+  if (variant > 0 && mode == kF32Acc64 && vec && !push) {
+    if (c <= 2) return pick_variant<2, 8>(variant, u_out);
+    if (c <= 4) return pick_variant<4, 4>(variant, u_out);
+    if (c <= 8) return pick_variant<8, 2>(variant, u_out);
+    return pick_variant<16, 1>(variant, u_out);
+  }
   switch (mode) {
     case kF32Acc64: return vec ? pick_cb<float, double, 16>(c, push) : pick_cb<float, double, 4>(c, push);
     case kF32Native: return vec ? pick_cb<float, float, 16>(c, push) : pick_cb<float, float, 4>(c, push);

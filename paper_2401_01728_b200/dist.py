@@ -44,6 +44,21 @@ def _close(device: int, ptr: int) -> None:
     N.load().rv_ipc_close(int(device), ctypes.c_void_p(int(ptr)))
 
 
+PUSH_MIN_BYTES = 32 << 20
+
+
+def choose_protocol(protocol: str, bytes_per_cluster: int) -> str:
+    """'auto': store-only push above 32 MiB per cluster (its per-unit flags
+    pay off and NVLink stores outrun loads: sweep_n4.jsonl), pull below (one
+    kernel round trip, no staging).  Depends only on the schedule and dtype,
+    so every rank picks the same protocol."""
+    if protocol == "auto":
+        return "push" if bytes_per_cluster >= PUSH_MIN_BYTES else "pull"
+    if protocol not in ("pull", "push"):
+        raise ConfigError(f"unknown protocol {protocol!r} (auto, pull or push)")
+    return protocol
+
+
 def rendezvous(mine: dict, group=None) -> tuple[list, list[int], int]:
     """All-gather each rank's descriptor (cluster id + IPC handles) and order
     ranks by ascending cluster id -- the ring member order (multiring.py:95).
@@ -71,7 +86,7 @@ class DistRingGroup:
 
     def __init__(self, schedule=None, src=None, dst=None, *, starts: Sequence[int] | None = None,
                  lens: Sequence[int] | None = None, cluster_id: int | None = None, acc: str = "f64",
-                 lanes: int = 1, group=None, timeout_s: float | None = None, protocol: str = "pull"):
+                 lanes: int = 1, group=None, timeout_s: float | None = None, protocol: str = "auto"):
         import torch.distributed as dist
 
         if src is None:
@@ -110,6 +125,7 @@ class DistRingGroup:
             self.plan.set_lanes(lanes)
         if timeout_s is not None:
             self.plan.set_timeout(timeout_s)
+        protocol = choose_protocol(protocol, total * src.element_size())
         self.protocol = protocol
         self.plan.set_protocol(protocol)
         flag_ptr, _ = self.plan.flag_area()
