@@ -260,48 +260,46 @@ __device__ __forceinline__ void fold_scalar(const CycleParams &p, const Seg &s, 
   for (int q = 0; q < p.C; ++q) __stcs(static_cast<T *>(p.dst[q]) + i, out);
 }
 
-// Fold vectors [jbeg, jend) of chunk s: every thread takes U vectors per
-// pass, loads all C members of each (U*C loads in flight), folds in ring
-// order, divides, and stores the mean into all C member buffers.
+// Fold one pass of chunk s: this thread takes vectors j0 + u*kThreads
+// (u < U, below jend), loads all C members of each (U*C loads in flight),
+// folds in ring order, divides, and stores the mean into all C buffers.
 template <typename T, typename Acc, int CB, int VB, int U, bool PUSH>
-__device__ __forceinline__ void fold_range(const CycleParams &p, const Seg &s, int64_t jbeg, int64_t jend) {
+__device__ __forceinline__ void fold_pass(const CycleParams &p, const Seg &s, int64_t j0, int64_t jend) {
   constexpr int N = VB / sizeof(T);
   using Raw = typename RawVec<VB>::type;
-  for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * U) {
-    Lanes<T, VB> x[U][CB];
+  Lanes<T, VB> x[U][CB];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + (int64_t)u * kThreads;
-      if (j < jend) {
-        const int64_t i = s.body_lo + j * N;
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = j0 + (int64_t)u * kThreads;
+    if (j < jend) {
+      const int64_t i = s.body_lo + j * N;
 #pragma unroll
-        for (int q = 0; q < CB; ++q) {
-          if (q < p.C) {
-            int m = s.k + q;
-            if (m >= p.C) m -= p.C;
-            x[u][q].raw = __ldcs(reinterpret_cast<const Raw *>(member_elem<T, PUSH>(p, s, m, i)));
-          }
+      for (int q = 0; q < CB; ++q) {
+        if (q < p.C) {
+          int m = s.k + q;
+          if (m >= p.C) m -= p.C;
+          x[u][q].raw = __ldcs(reinterpret_cast<const Raw *>(member_elem<T, PUSH>(p, s, m, i)));
         }
       }
     }
+  }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = j0 + (int64_t)u * kThreads;
-      if (j < jend) {
-        Lanes<T, VB> out;
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = j0 + (int64_t)u * kThreads;
+    if (j < jend) {
+      Lanes<T, VB> out;
 #pragma unroll
-        for (int e = 0; e < N; ++e) {
-          Acc acc = (Acc)x[u][0].v[e];
+      for (int e = 0; e < N; ++e) {
+        Acc acc = (Acc)x[u][0].v[e];
 #pragma unroll
-          for (int q = 1; q < CB; ++q)
-            if (q < p.C) acc = acc + (Acc)x[u][q].v[e];
-          out.v[e] = finish<T, Acc>(acc, p);
-        }
-        const int64_t i = s.body_lo + j * N;
-#pragma unroll
-        for (int q = 0; q < CB; ++q)
-          if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
+        for (int q = 1; q < CB; ++q)
+          if (q < p.C) acc = acc + (Acc)x[u][q].v[e];
+        out.v[e] = finish<T, Acc>(acc, p);
       }
+      const int64_t i = s.body_lo + j * N;
+#pragma unroll
+      for (int q = 0; q < CB; ++q)
+        if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
     }
   }
 }
@@ -311,9 +309,9 @@ __device__ __forceinline__ void fold_range(const CycleParams &p, const Seg &s, i
 // HBM or NVLink peer loads) and pushes the mean into every member.  Arrive
 // barrier first (peers' inputs final), depart barrier last.
 
-// MINB = 2 caps fp32 kernels at 128 registers (two 256-thread blocks per SM,
-// no spills); fp64 storage keeps its larger register set.
-template <typename T, typename Acc, int CB, int VB, int U, int MINB = (sizeof(T) == 4 ? 2 : 1)>
+// Two 256-thread blocks per SM (<= 128 registers): measured 1.18 ms vs
+// 1.47 ms at one block per SM on the co-resident BERT cycle.
+template <typename T, typename Acc, int CB, int VB, int U, int MINB = 2>
 __global__ void __launch_bounds__(kThreads, MINB)
 ring_cycle_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = VB / sizeof(T);
@@ -354,7 +352,7 @@ ring_cycle_kernel(const __grid_constant__ CycleParams p) {
       const int64_t local_tile = t - __ldg(p.tile_prefix + a);
       const int64_t nvec = (s.body_hi - s.body_lo) / N;
       const int64_t jbeg = local_tile * tile_vecs;
-      fold_range<T, Acc, CB, VB, U, false>(p, s, jbeg, min(nvec, jbeg + tile_vecs));
+      fold_pass<T, Acc, CB, VB, U, false>(p, s, jbeg + threadIdx.x, min(nvec, jbeg + tile_vecs));
       if (local_tile == 0) {
         const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
         if ((int64_t)threadIdx.x < nhead + ntail) {
@@ -395,10 +393,10 @@ __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
 }
 
 template <typename T, typename Acc, int CB, int VB, int U>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 ring_push_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = VB / sizeof(T);
-  constexpr int KC = (U * CB) < 16 ? (U * CB) : 16;  // vectors in flight per thread when copying
+  constexpr int KC = (U * CB) < 8 ? (U * CB) : 8;  // vectors in flight per thread when copying
   using Raw = typename RawVec<VB>::type;
   __shared__ int s_ok;
   __shared__ unsigned long long s_epoch;
@@ -468,8 +466,9 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
       if (!s_ok) break;
       const int64_t uu = u - s.unit0;
       const int64_t nvec = (s.body_hi - s.body_lo) / N;
-      const int64_t jbeg = uu * p.unit_vecs;
-      fold_range<T, Acc, CB, VB, U, true>(p, s, jbeg, min(nvec, jbeg + p.unit_vecs));
+      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
+      for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * U)
+        fold_pass<T, Acc, CB, VB, U, true>(p, s, j0, jend);
       if (uu == 0) {
         const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
         if ((int64_t)threadIdx.x < nhead + ntail) {
@@ -526,17 +525,35 @@ using KernelFn = void (*)(CycleParams);
 
 enum Mode { kF32Acc64 = 0, kF32Native = 1, kF64 = 2 };
 
+// Vectors per thread per pass: U*C 16-byte loads in flight, kept within the
+// 128-register budget (fp64 storage and the push kernel's staging addresses
+// take more registers, so they run at half U).
 template <typename T, typename Acc, int VB>
-KernelFn pick_cb(int c, bool push) {
-  if (c <= 2) return push ? ring_push_kernel<T, Acc, 2, VB, 8> : ring_cycle_kernel<T, Acc, 2, VB, 8>;
-  if (c <= 4) return push ? ring_push_kernel<T, Acc, 4, VB, 4> : ring_cycle_kernel<T, Acc, 4, VB, 4>;
-  if (c <= 8) return push ? ring_push_kernel<T, Acc, 8, VB, 2> : ring_cycle_kernel<T, Acc, 8, VB, 2>;
-  return push ? ring_push_kernel<T, Acc, 16, VB, 1> : ring_cycle_kernel<T, Acc, 16, VB, 1>;
+KernelFn pick_cb(int c, bool push, int *u_out) {
+  constexpr bool wide = sizeof(T) == 8;
+  if (push) {
+    if (c <= 2) { *u_out = 4; return ring_push_kernel<T, Acc, 2, VB, 4>; }
+    if (c <= 4) { *u_out = 2; return ring_push_kernel<T, Acc, 4, VB, 2>; }
+    if (c <= 8) { *u_out = 1; return ring_push_kernel<T, Acc, 8, VB, 1>; }
+    *u_out = 1;
+    return ring_push_kernel<T, Acc, 16, VB, 1>;
+  }
+  if constexpr (wide) {
+    if (c <= 2) { *u_out = 4; return ring_cycle_kernel<T, Acc, 2, VB, 4>; }
+    if (c <= 4) { *u_out = 2; return ring_cycle_kernel<T, Acc, 4, VB, 2>; }
+    if (c <= 8) { *u_out = 1; return ring_cycle_kernel<T, Acc, 8, VB, 1>; }
+  } else {
+    if (c <= 2) { *u_out = 8; return ring_cycle_kernel<T, Acc, 2, VB, 8>; }
+    if (c <= 4) { *u_out = 4; return ring_cycle_kernel<T, Acc, 4, VB, 4>; }
+    if (c <= 8) { *u_out = 2; return ring_cycle_kernel<T, Acc, 8, VB, 2>; }
+  }
+  *u_out = 1;
+  return ring_cycle_kernel<T, Acc, 16, VB, 1>;
 }
 
 // Tuning variants of the f32 / f64-fold vector pull kernel (RAVNEST_B200_VARIANT,
 // experiments only): 1 = half the vectors per thread, >= 3 blocks/SM;
-// 2 = half, >= 4 blocks/SM; 3 = same vectors, >= 1 block/SM (no register cap).
+// 2 = half, >= 4 blocks/SM; 3 = same vectors, no register cap (1 block/SM).
 template <int CB, int U>
 KernelFn pick_variant(int v, int *u_out) {
   constexpr int H = U > 1 ? U / 2 : 1;
@@ -549,7 +566,6 @@ KernelFn pick_variant(int v, int *u_out) {
 }
 
 KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
-  *u_out = c <= 2 ? 8 : c <= 4 ? 4 : c <= 8 ? 2 : 1;
   const char *ve = getenv("RAVNEST_B200_VARIANT");
   const int variant = ve ? atoi(ve) : 0;
   if (variant > 0 && mode == kF32Acc64 && vec && !push) {
@@ -559,9 +575,9 @@ KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
     return pick_variant<16, 1>(variant, u_out);
   }
   switch (mode) {
-    case kF32Acc64: return vec ? pick_cb<float, double, 16>(c, push) : pick_cb<float, double, 4>(c, push);
-    case kF32Native: return vec ? pick_cb<float, float, 16>(c, push) : pick_cb<float, float, 4>(c, push);
-    default: return vec ? pick_cb<double, double, 16>(c, push) : pick_cb<double, double, 8>(c, push);
+    case kF32Acc64: return vec ? pick_cb<float, double, 16>(c, push, u_out) : pick_cb<float, double, 4>(c, push, u_out);
+    case kF32Native: return vec ? pick_cb<float, float, 16>(c, push, u_out) : pick_cb<float, float, 4>(c, push, u_out);
+    default: return vec ? pick_cb<double, double, 16>(c, push, u_out) : pick_cb<double, double, 8>(c, push, u_out);
   }
 }
 
