@@ -9,7 +9,7 @@ CUDA, C ABI in include/ravnest_b200.h); importing this package does not need
 a GPU, calling the averaging functions does.
 """
 
-from .errors import ConfigError, LayoutError, ProtocolError, RavnestError, StallError
+from .errors import ConfigError, LayoutError, ProtocolError, RavnestError, SchemaError, StallError
 from .schedule import (
     CostReport,
     ParamRange,
@@ -35,6 +35,7 @@ __all__ = [
     "ParamRange",
     "ProtocolError",
     "RavnestError",
+    "SchemaError",
     "Ring",
     "RingCost",
     "RingSchedule",

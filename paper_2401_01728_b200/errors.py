@@ -28,3 +28,8 @@ class ProtocolError(RavnestError):
 class StallError(RavnestError):
     """A cycle could not complete: a peer never reached a barrier
     (multiring.py:296-298; here a device-side flag timeout)."""
+
+
+class SchemaError(RavnestError):
+    """A file whose schema tag or layout the reader does not accept
+    (configio.py:195-198, 505-510)."""

@@ -32,6 +32,7 @@ def _translate(ref_errors):
         _errors.LayoutError: getattr(ref_errors, "LayoutError", None),
         _errors.ProtocolError: getattr(ref_errors, "ProtocolError", None),
         _errors.StallError: getattr(ref_errors, "StallError", None),
+        _errors.SchemaError: getattr(ref_errors, "SchemaError", None),
         _errors.RavnestError: getattr(ref_errors, "RavnestError", None),
     }
 

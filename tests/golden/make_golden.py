@@ -177,6 +177,59 @@ def main():
     with open(os.path.join(HERE, "schedule_kats.json"), "w") as f:
         json.dump(kats, f, indent=1, sort_keys=True)
     print(f"wrote {len(names)} ring instances, {len(kats['schedules'])} schedule cases")
+    make_formats()
+
+
+def make_formats():
+    """Config 1 (BASELINE.json configs[0]): the reference's own session plan
+    for the MLP [3072,256,128,10] over two 3-peer clusters, serialised by
+    configio.serialize_plan; digests of apply_ring_mean on seeded inputs;
+    wire-frame and checkpoint golden bytes (multiring.py:400-426,
+    configio.py:495-512)."""
+    import hashlib
+    import tempfile
+
+    from ravnest import configio, modelcore
+    from ravnest.clusterform import ModelFootprint, plan_session
+    from ravnest.simnet import NodeSpec
+
+    arch = [3072, 256, 128, 10]
+    model, _ = modelcore.build_model(arch, 3, "tanh", "mse")
+    fp = ModelFootprint.from_model(model, 2)
+    pool, assignment = [], []
+    for ci, count in enumerate([3, 3], start=1):
+        for j in range(count):
+            pool.append(NodeSpec(f"c{ci}n{j}", fp.M, 1e9, 1.0))
+            assignment.append(ci)
+    plan = plan_session(pool, fp, 2, model, assignment=assignment)
+    text = configio.serialize_plan(plan)
+    with open(os.path.join(HERE, "config1_plan.txt"), "w") as f:
+        f.write(text)
+    out = {"ring_lengths": [r.length for r in plan.ring_schedule.rings], "total": plan.ring_schedule.total_params,
+           "cases": []}
+    for key in (1, 2):
+        rng = np.random.Generator(np.random.Philox(key=key))
+        vals = {cid: rng.normal(0.0, 1.0, plan.ring_schedule.total_params) for cid in plan.cluster_ids}
+        res = multiring.apply_ring_mean(plan.ring_schedule, vals)
+        out["cases"].append({
+            "philox_key": key, "clusters": plan.cluster_ids, "sigma": 1.0,
+            "sha256": {str(c): hashlib.sha256(res[c].astype("<f8").tobytes()).hexdigest() for c in res},
+            "first": {str(c): [float(v) for v in res[c][:4]] for c in res},
+        })
+    frames = []
+    for kind, rid, rnd, off, payload in (("ring_chunk", 1, 2, 3, [1.0]), ("ring_chunk", 7, 3, 160, [1.5, -2.25, 3.875]),
+                                         ("control", 0, 0, 0, [0.0, 0.0]), ("gradient", 4294967295, 5, 2**40, [-0.0, 5e-324])):
+        b = multiring.encode_frame(kind, rid, rnd, off, np.array(payload))
+        frames.append({"kind": kind, "ring_id": rid, "round": rnd, "offset": off, "payload": payload, "hex": b.hex()})
+    out["frames"] = frames
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "x.ckpt")
+        configio.write_checkpoint(path, np.array([1.0, -2.5, 3e-300]))
+        with open(path, "rb") as f:
+            out["checkpoint_hex"] = f.read().hex()
+    with open(os.path.join(HERE, "formats.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print("wrote config1_plan.txt, formats.json", out["ring_lengths"])
 
 
 if __name__ == "__main__":
