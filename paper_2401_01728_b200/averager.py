@@ -1,0 +1,115 @@
+"""Asynchronous periodic averaging for live training.
+
+The reference's global loop (orchestrator.py:302-337, Algorithm 2) counts
+parameter updates and, each time the count crosses a multiple of kappa,
+averages the clusters' parameters with the multi-ring all-reduce; batches
+still in flight then land their (stale) updates on the averaged parameters
+(pipeline.py:384-411).  On GPUs the averaging need not stop training:
+
+    every kappa updates  snap <- live           (training stream, HBM copy)
+                         mean <- ring mean(snap) (averaging stream, NVLink,
+                                                  overlaps further updates)
+    tau updates later    live <- mean + (live - snap)   (training stream)
+
+so the tau updates made while the cycle ran are applied on top of the
+average, exactly the reference's stale-update semantics with staleness tau.
+With tau = 0 the blend writes the mean itself (live == snap), i.e. the
+reference's synchronous snapshot barrier.  The cycle is one kernel per rank
+(DistRingGroup); with ``graph=True`` the snapshot copy and the cycle are
+captured once in a CUDA graph and replayed every kappa updates.
+"""
+
+from __future__ import annotations
+
+from .blend import blend_
+from .dist import DistRingGroup
+from .errors import ConfigError
+
+
+class AsyncAverager:
+    """One rank's side of periodic averaging over a torch.distributed group.
+
+    ``live`` is the rank's flat, contiguous CUDA parameter arena (the
+    optimizer updates it in place on ``train_stream``).  Call ``step()``
+    after every local update.
+    """
+
+    def __init__(self, live, schedule=None, *, starts=None, lens=None, kappa: int, tau: int = 0,
+                 cluster_id: int | None = None, acc: str = "f64", protocol: str = "auto",
+                 train_stream=None, graph: bool = False, group=None):
+        import torch
+
+        if kappa < 1:
+            raise ConfigError(f"kappa must be >= 1, got {kappa}")
+        if tau < 0 or tau >= kappa:
+            raise ConfigError(f"tau must be in [0, kappa), got {tau}")
+        self.live = live
+        self.snap = torch.empty_like(live)
+        self.mean = torch.empty_like(live)
+        self.kappa, self.tau = kappa, tau
+        self.train_stream = train_stream or torch.cuda.current_stream(live.device)
+        self.avg_stream = torch.cuda.Stream(device=live.device)
+        self.group = DistRingGroup(schedule, src=self.snap, dst=self.mean, starts=starts, lens=lens,
+                                   cluster_id=cluster_id, acc=acc, protocol=protocol, group=group)
+        self.t = 0
+        self.cycles = 0
+        self._pending_at = None
+        self._done = None
+        self._graph = None
+        self._use_graph = graph
+
+    def _launch(self):
+        import torch
+
+        # snapshot on the training stream: later updates cannot race the copy
+        self.snap.copy_(self.live)
+        self.avg_stream.wait_stream(self.train_stream)
+        if self._use_graph:
+            if self._graph is None:
+                # warm-up cycle builds the device tables; then capture one cycle
+                with torch.cuda.stream(self.avg_stream):
+                    self.group.average([self.avg_stream])
+                self.avg_stream.synchronize()
+                self._graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self._graph, stream=self.avg_stream):
+                    self.group.average([self.avg_stream])
+                # the capture itself did not run the cycle
+            with torch.cuda.stream(self.avg_stream):
+                self._graph.replay()
+        else:
+            self.group.average([self.avg_stream])
+        self._done = torch.cuda.Event()
+        self._done.record(self.avg_stream)
+
+    def _finish(self):
+        self.train_stream.wait_event(self._done)
+        blend_(self.live, self.snap, self.mean, self.train_stream)
+        self._pending_at = None
+        self.cycles += 1
+
+    def step(self) -> bool:
+        """Count one local update; start or finish a cycle when due.
+        Returns True when a blend was issued at this step."""
+        self.t += 1
+        finished = False
+        if self._pending_at is not None and self.t >= self._pending_at + self.tau:
+            self._finish()
+            finished = True
+        if self.t % self.kappa == 0 and self._pending_at is None:
+            self._launch()
+            self._pending_at = self.t
+            if self.tau == 0:
+                self._finish()
+                finished = True
+        return finished
+
+    def flush(self) -> None:
+        """Finish a pending cycle now (end of training)."""
+        if self._pending_at is not None:
+            self._finish()
+
+    def close(self) -> None:
+        self.flush()
+        self.train_stream.synchronize()
+        self._graph = None
+        self.group.close()

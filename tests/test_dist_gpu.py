@@ -24,3 +24,17 @@ def test_dist_ring_group_parity():
     out = res.stdout + res.stderr
     assert res.returncode == 0, out[-4000:]
     assert f"DIST OK world={n}" in out, out[-4000:]
+
+
+def test_async_averager_matches_reference_semantics():
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    n = torch.cuda.device_count()
+    env = dict(os.environ, RAVNEST_B200_TIMEOUT_S="10")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29534",
+           os.path.join(ROOT, "tests", "dist_averager_worker.py")]
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    out = res.stdout + res.stderr
+    assert res.returncode == 0, out[-4000:]
+    assert f"AVERAGER OK world={n}" in out, out[-4000:]
