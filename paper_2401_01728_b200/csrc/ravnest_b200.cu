@@ -483,6 +483,179 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
   depart(p, epoch);
 }
 
+// ---------------------------------------------------------------------------
+// co-resident TMA path (all C members on this device, 16-byte congruent
+// buffers): HBM-bound, so tiles stream through shared memory with bulk async
+// copies.  Warp 0 / lane 0 produces: for each tile it loads the tile of all C
+// members (cp.async.bulk global->shared, completion on a per-stage mbarrier)
+// into a STAGES-deep ring.  Warps 1..8 consume: fold from shared memory in
+// ring order, write the mean tile to shared memory, and one consumer issues
+// C bulk stores (shared->global) of it, double-buffered.  No register
+// staging of loads, so each SM keeps STAGES * C * TV * 16 bytes in flight.
+
+constexpr int kTmaConsumers = 256;
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *smem, const void *gmem, unsigned bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <typename T, typename Acc, int CB, int TV, int STAGES>
+__global__ void __launch_bounds__(kTmaConsumers + 32, 1)
+ring_tma_kernel(const __grid_constant__ CycleParams p) {
+  constexpr int N = 16 / sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][CB][TV]
+  uint4 *out = in + (size_t)STAGES * CB * TV;                          // [2][TV]
+  __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x;
+  const int C = p.C;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    trace_min(p, 0);
+    trace_max(p, 1);
+  }
+  __syncthreads();
+
+  // the tiles this block owns: t = blockIdx.x + i * gridDim.x
+  auto seg_of = [&](int64_t t, int64_t *local) -> Seg {
+    int a = 0, b = p.nseg - 1;
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
+    }
+    *local = t - __ldg(p.tile_prefix + a);
+    return p.segs[a];
+  };
+
+  if (tid < 32) {
+    if (tid == 0) {  // producer
+      int stage = 0;
+      unsigned phase = 0;
+      int64_t n = 0;
+      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++n) {
+        int64_t lt;
+        const Seg s = seg_of(t, &lt);
+        const int64_t nvec = (s.body_hi - s.body_lo) / N;
+        const int64_t j0 = lt * TV;
+        const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
+        if (n >= STAGES) mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], (unsigned)(cnt * 16 * C));
+        if (cnt > 0) {
+          for (int q = 0; q < C; ++q) {
+            int m = s.k + q;
+            if (m >= C) m -= C;
+            bulk_load(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
+                      (unsigned)(cnt * 16), &full[stage]);
+          }
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // consumers (256 threads)
+  const int c = tid - 32;
+  int stage = 0;
+  unsigned phase = 0;
+  int ob = 0;
+  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+    int64_t lt;
+    const Seg s = seg_of(t, &lt);
+    const int64_t nvec = (s.body_hi - s.body_lo) / N;
+    const int64_t j0 = lt * TV;
+    const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
+    mbar_wait(&full[stage], phase);
+    // consumer 0 finished the previous tile's store bookkeeping (out[ob] free)
+    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+    for (int v = c; v < cnt; v += kTmaConsumers) {
+      Lanes<T, 16> x, o;
+      Acc acc[N];
+      x.raw = in[((size_t)stage * CB + 0) * TV + v];
+#pragma unroll
+      for (int e = 0; e < N; ++e) acc[e] = (Acc)x.v[e];
+#pragma unroll
+      for (int q = 1; q < CB; ++q) {
+        if (q < C) {
+          x.raw = in[((size_t)stage * CB + q) * TV + v];
+#pragma unroll
+          for (int e = 0; e < N; ++e) acc[e] = acc[e] + (Acc)x.v[e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < N; ++e) o.v[e] = finish<T, Acc>(acc[e], p);
+      out[ob * TV + v] = o.raw;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+    if (c == 0) {
+      mbar_arrive(&empty[stage]);  // every consumer has read this stage
+      if (cnt > 0) {
+        for (int q = 0; q < C; ++q)
+          bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // out[ob ^ 1] reusable
+    }
+    if (lt == 0) {
+      const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+      if ((int64_t)c < nhead + ntail) {
+        const int64_t i = (int64_t)c < nhead ? s.lo + c : s.body_hi + ((int64_t)c - nhead);
+        fold_scalar<T, Acc, false>(p, s, i);
+      }
+    }
+    ob ^= 1;
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  if (c == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    trace_max(p, 2);
+  }
+}
+
 // live <- mean + (live - snap); exactly mean where live == snap bitwise.
 template <typename T, typename U>
 __global__ void __launch_bounds__(kThreads)
@@ -563,6 +736,29 @@ KernelFn pick_variant(int v, int *u_out) {
     case 3: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 1>;
     default: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 2>;
   }
+}
+
+// Co-resident TMA kernel: 32 KB of member data per pipeline stage
+// (CB * TV * 16 bytes), 4 stages.
+constexpr int kTmaStages = 4;
+constexpr int kTmaStageBytes = 32 * 1024;
+
+template <typename T, typename Acc>
+KernelFn pick_tma(int c, int *tv_out) {
+  if (c <= 2) { *tv_out = kTmaStageBytes / (2 * 16); return ring_tma_kernel<T, Acc, 2, kTmaStageBytes / (2 * 16), kTmaStages>; }
+  if (c <= 4) { *tv_out = kTmaStageBytes / (4 * 16); return ring_tma_kernel<T, Acc, 4, kTmaStageBytes / (4 * 16), kTmaStages>; }
+  if (c <= 8) { *tv_out = kTmaStageBytes / (8 * 16); return ring_tma_kernel<T, Acc, 8, kTmaStageBytes / (8 * 16), kTmaStages>; }
+  *tv_out = kTmaStageBytes / (16 * 16);
+  return ring_tma_kernel<T, Acc, 16, kTmaStageBytes / (16 * 16), kTmaStages>;
+}
+
+KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
+  KernelFn k = mode == kF32Acc64 ? pick_tma<float, double>(c, tv_out)
+             : mode == kF32Native ? pick_tma<float, float>(c, tv_out)
+                                  : pick_tma<double, double>(c, tv_out);
+  const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
+  *smem_out = (size_t)kTmaStages * cb * (*tv_out) * 16 + 2 * (size_t)(*tv_out) * 16;
+  return k;
 }
 
 KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
@@ -662,6 +858,8 @@ struct rv_plan {
   KernelFn kernel = nullptr;
   int occ = 0;
   bool use_push = false;
+  int block_threads = kThreads;
+  size_t smem_bytes = 0;
 };
 
 namespace {
@@ -762,11 +960,24 @@ int build_tables(rv_plan *p) {
   p->use_push = push;
   const int mode = p->dtype == RV_DTYPE_F64 ? kF64 : (p->acc == RV_ACC_NATIVE ? kF32Native : kF32Acc64);
   int U = 1;
-  p->kernel = pick_kernel(mode, p->C, vec, push, &U);
+  int64_t tile_vecs = 0;
   DeviceGuard g(p->device);
-  RV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ, p->kernel, kThreads, 0));
+  const char *tma_env = getenv("RAVNEST_B200_TMA");
+  const bool tma = vec && p->n_ranks == 1 && !(tma_env && tma_env[0] == '0');
+  if (tma) {
+    int tv = 0;
+    p->kernel = pick_tma_kernel(mode, p->C, &tv, &p->smem_bytes);
+    p->block_threads = kTmaConsumers + 32;
+    RV_CUDA(cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem_bytes));
+    tile_vecs = tv;
+  } else {
+    p->kernel = pick_kernel(mode, p->C, vec, push, &U);
+    p->block_threads = kThreads;
+    p->smem_bytes = 0;
+    tile_vecs = (int64_t)kThreads * U;
+  }
+  RV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ, p->kernel, p->block_threads, p->smem_bytes));
   if (p->occ < 1) p->occ = 1;
-  const int64_t tile_vecs = (int64_t)kThreads * U;
   // push: unit size adapts so that a cycle has >= ~2 work items per resident
   // block (small shards stay parallel, large ones amortise the unit flags);
   // it depends only on the schedule and the device model, so every rank
@@ -929,7 +1140,7 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
   }
   if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet
   const int grid = std::max(1, lane.grid);
-  p->kernel<<<grid, kThreads, 0, st>>>(cp);
+  p->kernel<<<grid, p->block_threads, p->smem_bytes, st>>>(cp);
   RV_CUDA(cudaGetLastError());
   return RV_OK;
 }
