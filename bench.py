@@ -129,8 +129,8 @@ def busbw(total_params: int, c: int, seconds: float) -> float:
 
 
 class CpuSample:
-    """A bounded sample of the workload for the CPU oracle: the first `frac`
-    of every ring (same C, same ring structure), fp32 N(0, 0.02)."""
+    """A bounded sample of the workload for the CPU legs: the first `frac` of
+    every ring (same C, same ring structure), fp32 N(0, 0.02)."""
 
     def __init__(self, lens, c: int, budget_params: int):
         import numpy as np
@@ -144,9 +144,23 @@ class CpuSample:
         self.xs = [rng.standard_normal(self.total, dtype=np.float32) * np.float32(SIGMA) for _ in range(c)]
         self.outs = [np.empty_like(x) for x in self.xs]
 
-    def run(self, threads: int) -> float:
-        """One cycle of the C oracle (f32 in, f64 fold, f32 out -- the product
-        contract); returns seconds."""
+    def run_port(self) -> float:
+        """One cycle of the reference's own algorithm, ported faithfully: the
+        round-by-round ring of apply_ring_mean (multiring.py:302-333) in numpy
+        float64 with its copy-in and payload copies (oracle/ring_oracle.py
+        ring_mean_rounds).  numpy ufuncs are single-threaded, like the
+        reference.  Returns seconds."""
+        import numpy as np
+
+        from oracle import ring_oracle
+
+        t0 = time.perf_counter()
+        ring_oracle.ring_mean_rounds(ring_starts(self.lens), self.lens, self.xs, dtype=np.float64)
+        return time.perf_counter() - t0
+
+    def run_threaded(self, threads: int) -> float:
+        """One cycle of the closed-form C oracle on `threads` host threads
+        (f32 in, f64 fold, f32 out -- the product contract); seconds."""
         from oracle import c_oracle
 
         t0 = time.perf_counter()
@@ -155,10 +169,24 @@ class CpuSample:
         return time.perf_counter() - t0
 
 
-def cpu_oracle_time(lens, c: int, budget_params: int, threads: int, repeats: int = 1):
-    smp = CpuSample(lens, c, budget_params)
-    smp.run(threads)
-    return smp.total, [smp.run(threads) for _ in range(repeats)]
+def cpu_legs(lens, c: int, port_params: int, threaded_params: int, threads: int):
+    """(reference-port record, threaded-oracle record) for cpu_baseline."""
+    port = CpuSample(lens, c, port_params)
+    port.run_port()
+    tp = min(port.run_port() for _ in range(2))
+    thr = CpuSample(lens, c, threaded_params)
+    thr.run_threaded(threads)
+    tt = min(thr.run_threaded(threads) for _ in range(3))
+    total = sum(lens)
+    return (
+        {"value": round(busbw(port.total, c, tp), 4), "unit": "GB/s", "cores": 1, "kind": "port",
+         "sample": f"first {port.total} of {total} params per cluster (every ring scaled), C={c}; "
+                   f"reference algorithm ported round by round (numpy fp64, single-threaded like the "
+                   f"reference), best of 2, {cpu_model()}"},
+        {"value": round(busbw(thr.total, c, tt), 3), "unit": "GB/s", "cores": threads, "kind": "oracle-c",
+         "sample": f"first {thr.total} of {total} params per cluster, C={c}; closed-form C oracle, "
+                   f"{threads} threads, best of 3"},
+    )
 
 
 def host_threads() -> int:
@@ -180,32 +208,32 @@ def cpu_model() -> str:
 
 
 def run_reference(args, n_gpus: int, rank: int):
+    """--impl reference: the reference's own algorithm (faithful numpy port of
+    apply_ring_mean, single-threaded like the reference) on a bounded sample
+    of the same workload, rank 0 only."""
     if rank != 0:
         return
     lens = WORKLOADS[args.workload]
     c = args.clusters or (8 if n_gpus == 1 else n_gpus)
-    threads = host_threads()
-    budget = args.cpu_sample_params
-    smp = CpuSample(lens, c, budget)
-    s_total = smp.total
+    smp = CpuSample(lens, c, args.ref_sample_params)
     for _ in range(args.warmup):
-        smp.run(threads)
-    steps = [smp.run(threads) for _ in range(args.steps)]
+        smp.run_port()
+    steps = [smp.run_port() for _ in range(args.steps)]
     t = statistics.median(steps)
-    bw = busbw(s_total, c, t)
-    value = bw * n_gpus
+    value = busbw(smp.total, c, t) * n_gpus
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * 1e3 * sum(lens) / s_total, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 fold)",
-        "data": "synthetic N(0,0.02) fp32, Philox seeded",
+        "ms_per_step": round(t * 1e3 * sum(lens) / smp.total, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference arithmetic)",
+        "data": "synthetic N(0,0.02) fp32 widened to fp64 like the reference, Philox seeded",
         "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
-                   "parallelism": f"cpu threads {threads}"},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"first {s_total} of {sum(lens)} params per cluster (every ring scaled), "
-                                   f"C={c}, oracle/ring_oracle.c f32-in f64-fold, {cpu_model()}"},
-        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "parallelism": "1 host thread (numpy ufuncs, as the reference)"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": f"first {smp.total} of {sum(lens)} params per cluster (every ring scaled), "
+                                   f"C={c}, round-by-round numpy port of multiring.apply_ring_mean "
+                                   f"(oracle/ring_oracle.ring_mean_rounds), {cpu_model()}"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -365,10 +393,10 @@ def run_single(args):
     achieved = hbm_bytes / (kernel_ms * 1e-3) / 1e9
     bw = busbw(total, c, ms * 1e-3)
 
-    # CPU baseline: the oracle port on a bounded sample, all host threads
+    # CPU baselines on bounded samples: the reference algorithm (faithful
+    # port, 1 thread) and the closed-form C oracle on every host thread
     threads = host_threads()
-    s_total, ct = cpu_oracle_time(lens, c, args.cpu_sample_params, threads, repeats=3)
-    cpu_bw = busbw(s_total, c, min(ct))
+    cpu_port, cpu_threaded = cpu_legs(lens, c, args.ref_sample_params, args.cpu_sample_params, threads)
 
     line = {
         "metric": METRIC, "value": round(bw, 3), "unit": "GB/s", "n_gpus": 1,
@@ -386,9 +414,8 @@ def run_single(args):
                      "frac": round(achieved / hbm_peak, 4), "traffic": None,
                      "basis": f"2*C*S = {hbm_bytes} B per launch (read C, write C vectors)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
-        "cpu_baseline": {"value": round(cpu_bw, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"first {s_total} of {total} params per cluster, C={c}, "
-                                   f"oracle/ring_oracle.c, best of 3, {cpu_model()}"},
+        "cpu_baseline": cpu_port,
+        "cpu_threaded": cpu_threaded,
         "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3), 3), "unit": "GB/s",
                 "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": c * total * 4, "d2h_bytes_per_step": c * total * 4,
@@ -575,6 +602,7 @@ def main():
     ap.add_argument("--protocol", choices=["auto", "pull", "push"], default="auto")
     ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")
     ap.add_argument("--cpu-sample-params", type=int, default=8_000_000)
+    ap.add_argument("--ref-sample-params", type=int, default=2_000_000)
     ap.add_argument("--nccl", type=int, default=1)
     ap.add_argument("--blend", type=int, default=0, help="config 4: snapshot average + delayed-update blend")
     ap.add_argument("--tau", type=int, default=4)

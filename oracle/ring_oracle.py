@@ -127,13 +127,13 @@ def ring_mean_rounds(
                 posts.append((k, work[m][lo:hi].copy()))
             for m, (k, payload) in enumerate(posts):
                 lo, hi = bounds[k]
-                dst = work[(m + 1) % c]
+                seg = work[(m + 1) % c][lo:hi]  # view: the updates land in place
                 if reduce_phase:
-                    dst[lo:hi] = dst[lo:hi] + payload
+                    seg += payload
                     if rnd == c - 2:
-                        dst[lo:hi] = dst[lo:hi] / dtype(c)
+                        seg /= dtype(c)
                 else:
-                    dst[lo:hi] = payload
+                    seg[...] = payload
     return work
 
 

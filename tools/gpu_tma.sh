@@ -2,10 +2,11 @@
 set -u
 mkdir -p gpurun_out
 export RAVNEST_B200_TIMEOUT_S=10
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_gpu.log
-for tma in 1 0; do
-  RAVNEST_B200_TMA=$tma timeout 300 python bench.py --steps 40 --warmup 5 > gpurun_out/tma_$tma.log 2>&1
-  echo "N1 tma=$tma rc=$? $(grep -o '"avg_kernel_ms": [0-9.]*' gpurun_out/tma_$tma.log) $(grep -o '"frac": [0-9.]*' gpurun_out/tma_$tma.log)"
-  RAVNEST_B200_TMA=$tma timeout 300 python bench.py --steps 20 --warmup 5 --workload resnet50 > gpurun_out/tma_r_$tma.log 2>&1
-  echo "N1 resnet tma=$tma rc=$? $(grep -o '"avg_kernel_ms": [0-9.]*' gpurun_out/tma_r_$tma.log) $(grep -o '"frac": [0-9.]*' gpurun_out/tma_r_$tma.log)"
+for v in 0 1 2 3; do
+  for rep in 1 2; do
+  RAVNEST_B200_TMA_VARIANT=$v timeout 300 python bench.py --steps 50 --warmup 5 > gpurun_out/tmav_$v.log 2>&1
+  echo "N1 tma variant=$v rc=$? $(grep -o '"avg_kernel_ms": [0-9.]*' gpurun_out/tmav_$v.log) $(grep -o '"frac": [0-9.]*' gpurun_out/tmav_$v.log)"
+  done
 done
+RAVNEST_B200_TMA=0 timeout 300 python bench.py --steps 50 --warmup 5 > gpurun_out/tma_0.log 2>&1
+echo "N1 no-tma rc=$? $(grep -o '"avg_kernel_ms": [0-9.]*' gpurun_out/tma_0.log) $(grep -o '"frac": [0-9.]*' gpurun_out/tma_0.log)"
