@@ -112,6 +112,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(workload: str, c: int, n_gpus: int, acc: str):
+    """Per-launch DRAM bytes of the dominant kernel from a committed ncu
+    capture of the same configuration (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            entry = json.load(f).get(f"{workload}/c{c}/n{n_gpus}/{acc}")
+        return entry["bytes"] if entry else None
+    except Exception:
+        return None
+
+
 def ring_starts(lens):
     out, s = [], 0
     for n in lens:
@@ -411,7 +422,8 @@ def run_single(args):
                    "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
                    "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "frac": round(achieved / hbm_peak, 4),
+                     "traffic": ncu_traffic(args.workload, c, 1, args.acc) if not args.blend else None,
                      "basis": f"2*C*S = {hbm_bytes} B per launch (read C, write C vectors)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
         "cpu_baseline": cpu_port,

@@ -13,7 +13,7 @@ from collections import defaultdict
 
 
 def short(name: str) -> str:
-    m = re.search(r"(ring_cycle_kernel<[^>]*>|blend_kernel\w*<[^>]*>)", name)
+    m = re.search(r"(ring_\w+_kernel<[^>]*>|blend_kernel\w*<[^>]*>)", name)
     if m:
         return m.group(1)
     return name.split("(")[0][-90:]
@@ -35,7 +35,7 @@ def launches(path: str, out: str) -> None:
         agg[k][0] += 1
         agg[k][1] += ns
     total = sum(v[1] for v in agg.values())
-    ours = sum(v[1] for k, v in agg.items() if "ring_cycle" in k or "blend" in k)
+    ours = sum(v[1] for k, v in agg.items() if k.startswith("ring_") or "blend" in k)
     with open(out, "w") as f:
         f.write(f"# ncu launch list summary ({path})\n\n")
         f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over the whole program "
@@ -44,9 +44,9 @@ def launches(path: str, out: str) -> None:
         f.write("| kernel | launches | total ms | mean us |\n|---|---|---|---|\n")
         for k, (n, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             f.write(f"| `{k}` | {n} | {ns / 1e6:.3f} | {ns / n / 1e3:.1f} |\n")
-        ring = [r for r in rows if "ring_cycle" in r[1]]
+        ring = [r for r in rows if r[1].startswith("ring_")]
         if ring:
-            f.write("\nring_cycle launches (in order): " + ", ".join(f"{r[3] / 1e3:.1f}us" for r in ring) + "\n")
+            f.write("\nring kernel launches (in order): " + ", ".join(f"{r[3] / 1e3:.1f}us" for r in ring) + "\n")
     print(open(out).read())
 
 
