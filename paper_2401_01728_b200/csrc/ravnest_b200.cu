@@ -849,6 +849,7 @@ struct rv_plan {
   int push_lanes = 0;
   std::vector<char *> peer_push;  // by rank
   unsigned long long *trace = nullptr;  // lanes x 4, when tracing
+  std::vector<cudaEvent_t> h2d_done;    // host-buffer pipeline, one per lane
   // built lane tables
   bool dirty = true;       // local positions / lanes / peers / protocol changed
   bool ptrs_dirty = true;  // buffers rebound: rebuild only if the alignment class changed
@@ -1391,9 +1392,18 @@ int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const 
     if (rc) return rc;
   }
   const int es = elem_size(p->dtype);
+  // host->device copies run lane after lane (lane l's kernel starts as soon
+  // as its own inputs have landed, while lane l+1's copy streams in and lane
+  // l-1's result streams out): a three-stage H2D / average / D2H pipeline
+  while ((int)p->h2d_done.size() < p->n_lanes) {
+    cudaEvent_t e;
+    RV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->h2d_done.push_back(e);
+  }
   for (int l = 0; l < p->n_lanes; ++l) {
     cudaStream_t st = (streams && n_streams > 0) ? (cudaStream_t)streams[l % n_streams] : (cudaStream_t)0;
     const auto &rings = p->lanes[l].rings;
+    if (l > 0) RV_CUDA(cudaStreamWaitEvent(st, p->h2d_done[l - 1], 0));
     for (size_t i = 0; i < p->local.size(); ++i) {
       const int pos = p->local[i];
       for (int r : rings) {
@@ -1403,6 +1413,7 @@ int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const 
                                 cudaMemcpyHostToDevice, st));
       }
     }
+    RV_CUDA(cudaEventRecord(p->h2d_done[l], st));
     int rc = launch_lane(p, l, st);
     if (rc) return rc;
     for (size_t i = 0; i < p->local.size(); ++i) {
@@ -1454,6 +1465,7 @@ int rv_plan_destroy(rv_plan *p) {
     free_lanes(p);
     if (p->push_area) cudaFree(p->push_area);
     if (p->trace) cudaFree(p->trace);
+    for (cudaEvent_t e : p->h2d_done) cudaEventDestroy(e);
     if (p->flags) cudaFree(p->flags);
     if (p->states) cudaFree(p->states);
     if (p->status) cudaFree(p->status);
