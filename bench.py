@@ -457,7 +457,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
         live = stale_live(x, rank, args.tau)
         mean = torch.empty_like(x)
     grp = DistRingGroup(src=x, dst=mean, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes,
-                        protocol=args.protocol)
+                        protocol=args.protocol, max_blocks=args.max_blocks)
     stream = torch.cuda.current_stream()
     lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
 
@@ -548,6 +548,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
             "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                        "placement": "one cluster per GPU", "lanes": args.lanes, "protocol": grp.protocol,
+                       "max_blocks": args.max_blocks or None,
                        "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
                        "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
                        "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
@@ -611,6 +612,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert")
     ap.add_argument("--acc", choices=["f64", "native"], default="f64")
     ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--max-blocks", type=int, default=0, help="cap resident blocks of the cycle (0 = all SMs)")
     ap.add_argument("--protocol", choices=["auto", "pull", "push"], default="auto")
     ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")
     ap.add_argument("--cpu-sample-params", type=int, default=8_000_000)

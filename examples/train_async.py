@@ -38,7 +38,7 @@ def build(width: int, depth: int, dev):
     return torch.nn.Sequential(*layers).to(dev)
 
 
-def run(regime: str, args, rank: int, dev):
+def run(regime: str, args, rank: int, dev, sm_budget: int = 0):
     torch.manual_seed(1234)  # same init on every rank (as the reference's clusters)
     model = build(args.width, args.depth, dev)
     arena = ParamArena(model, grads=True)
@@ -48,7 +48,7 @@ def run(regime: str, args, rank: int, dev):
     if regime != "none":
         tau = 0 if regime == "sync" else args.tau
         avg = AsyncAverager(arena.flat, starts=starts, lens=lengths, kappa=args.kappa, tau=tau,
-                            graph=args.graph)
+                            graph=args.graph, sm_budget=sm_budget)
     g = torch.Generator(device=dev).manual_seed(100 + rank)
     x = torch.randn(args.batch, args.width, device=dev, generator=g)
     y = torch.randint(0, 10, (args.batch,), device=dev, generator=g)
@@ -58,6 +58,8 @@ def run(regime: str, args, rank: int, dev):
         arena.grad.zero_()
         loss = loss_fn(model(x), y)
         loss.backward()
+        if avg is not None:
+            avg.before_update()
         arena.flat.add_(arena.grad, alpha=-args.lr)  # one fused SGD update on the arena
         if avg is not None:
             avg.step()
@@ -96,22 +98,27 @@ def main():
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--lr", type=float, default=1e-3)
     ap.add_argument("--graph", type=int, default=0)
+    ap.add_argument("--sm-budgets", default="16,32,64,0", help="SM budgets of the async cycle (0 = all)")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
-    res = {r: run(r, args, rank, dev) for r in ("none", "sync", "async")}
+    budgets = [int(b) for b in args.sm_budgets.split(",")]
+    res = {"none": run("none", args, rank, dev), "sync": run("sync", args, rank, dev, 0)}
+    for b in budgets:
+        res[f"async_sm{b}"] = run("async", args, rank, dev, b)
     if rank == 0:
-        base, sync, asyn = (res[k]["ms_per_step"] for k in ("none", "sync", "async"))
+        base, sync = res["none"]["ms_per_step"], res["sync"]["ms_per_step"]
         cycle_cost = (sync - base) * args.kappa  # ms a cycle adds when it is on the critical path
-        hidden = 1.0 - (asyn - base) / max(sync - base, 1e-9)
+        hidden = {b: round(1.0 - (res[f"async_sm{b}"]["ms_per_step"] - base) / max(sync - base, 1e-9), 3)
+                  for b in budgets}
         print(json.dumps({
             "example": "train_async", "n_gpus": world, "params_per_cluster": res["none"]["params"],
             "kappa": args.kappa, "tau": args.tau, "rings": args.rings, "results": res,
             "cycle_ms_on_critical_path": round(cycle_cost, 4),
-            "fraction_of_averaging_hidden_by_async": round(hidden, 3),
+            "fraction_of_averaging_hidden_by_async": hidden,
         }), flush=True)
     dist.destroy_process_group()
 

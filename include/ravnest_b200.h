@@ -114,6 +114,11 @@ int rv_plan_set_push_peers(rv_plan *plan, void *const *areas);
 
 int rv_plan_set_timeout(rv_plan *plan, double seconds);
 
+/* Cap the blocks a cycle keeps resident (0 = whole device).  An NVLink-bound
+ * cycle needs only part of the SMs; the rest stay free for training kernels
+ * running concurrently on other streams. */
+int rv_plan_set_max_blocks(rv_plan *plan, int max_blocks);
+
 /* Phase tracing (off by default): per lane, the device globaltimer (ns) of
  * [earliest block start, last block ready for data (pull: arrive barrier
  * passed), last block done with data, depart barrier completed] of the most

@@ -6,8 +6,8 @@ averages the clusters' parameters with the multi-ring all-reduce; batches
 still in flight then land their (stale) updates on the averaged parameters
 (pipeline.py:384-411).  On GPUs the averaging need not stop training:
 
-    every kappa updates  snap <- live           (training stream, HBM copy)
-                         mean <- ring mean(snap) (averaging stream, NVLink,
+    every kappa updates  snap <- live           (side stream, HBM copy)
+                         mean <- ring mean(snap) (side stream, NVLink,
                                                   overlaps further updates)
     tau updates later    live <- mean + (live - snap)   (training stream)
 
@@ -15,8 +15,15 @@ so the tau updates made while the cycle ran are applied on top of the
 average, exactly the reference's stale-update semantics with staleness tau.
 With tau = 0 the blend writes the mean itself (live == snap), i.e. the
 reference's synchronous snapshot barrier.  The cycle is one kernel per rank
-(DistRingGroup); with ``graph=True`` the snapshot copy and the cycle are
-captured once in a CUDA graph and replayed every kappa updates.
+(DistRingGroup); with ``graph=True`` it is captured once in a CUDA graph and
+replayed every kappa updates.
+
+Overlap: the cycle runs on a high-priority side stream with an SM budget
+(``sm_budget`` SMs; NVLink-bound, it does not need the whole GPU), so the
+training kernels keep the remaining SMs.  The snapshot copy also runs on the
+side stream; only the next parameter update has to wait for it -- call
+``before_update()`` right before the optimizer writes ``live`` (forward and
+backward of the next step overlap the copy).
 """
 
 from __future__ import annotations
@@ -36,7 +43,7 @@ class AsyncAverager:
 
     def __init__(self, live, schedule=None, *, starts=None, lens=None, kappa: int, tau: int = 0,
                  cluster_id: int | None = None, acc: str = "f64", protocol: str = "auto",
-                 train_stream=None, graph: bool = False, group=None):
+                 train_stream=None, graph: bool = False, group=None, sm_budget: int = 32):
         import torch
 
         if kappa < 1:
@@ -48,22 +55,28 @@ class AsyncAverager:
         self.mean = torch.empty_like(live)
         self.kappa, self.tau = kappa, tau
         self.train_stream = train_stream or torch.cuda.current_stream(live.device)
-        self.avg_stream = torch.cuda.Stream(device=live.device)
+        self.avg_stream = torch.cuda.Stream(device=live.device, priority=-1)
         self.group = DistRingGroup(schedule, src=self.snap, dst=self.mean, starts=starts, lens=lens,
-                                   cluster_id=cluster_id, acc=acc, protocol=protocol, group=group)
+                                   cluster_id=cluster_id, acc=acc, protocol=protocol, group=group,
+                                   max_blocks=2 * sm_budget if sm_budget else 0)
         self.t = 0
         self.cycles = 0
         self._pending_at = None
         self._done = None
+        self._snapped = None
         self._graph = None
         self._use_graph = graph
 
     def _launch(self):
         import torch
 
-        # snapshot on the training stream: later updates cannot race the copy
-        self.snap.copy_(self.live)
+        # snapshot on the side stream, after everything training has issued;
+        # before_update() keeps the next write to `live` behind the copy
         self.avg_stream.wait_stream(self.train_stream)
+        with torch.cuda.stream(self.avg_stream):
+            self.snap.copy_(self.live)
+        self._snapped = torch.cuda.Event()
+        self._snapped.record(self.avg_stream)
         if self._use_graph:
             if self._graph is None:
                 # warm-up cycle builds the device tables; then capture one cycle
@@ -82,10 +95,18 @@ class AsyncAverager:
         self._done.record(self.avg_stream)
 
     def _finish(self):
+        self.before_update()
         self.train_stream.wait_event(self._done)
         blend_(self.live, self.snap, self.mean, self.train_stream)
         self._pending_at = None
         self.cycles += 1
+
+    def before_update(self) -> None:
+        """Call right before the optimizer writes ``live``: orders that write
+        after a pending snapshot copy (no-op otherwise)."""
+        if self._snapped is not None:
+            self.train_stream.wait_event(self._snapped)
+            self._snapped = None
 
     def step(self) -> bool:
         """Count one local update; start or finish a cycle when due.

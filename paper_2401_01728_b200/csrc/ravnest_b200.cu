@@ -874,6 +874,7 @@ struct rv_plan {
   bool use_push = false;
   int block_threads = kThreads;
   size_t smem_bytes = 0;
+  int max_blocks = 0;  // 0 = whole device; else cap on resident blocks (SM budget)
 };
 
 namespace {
@@ -1099,7 +1100,8 @@ int build_tables(rv_plan *p) {
   }
   // persistent grid: all lanes together fit in one wave (no lane can starve
   // another on this device while both wait on peers)
-  const int64_t capacity = (int64_t)p->sm_count * p->occ;
+  int64_t capacity = (int64_t)p->sm_count * p->occ;
+  if (p->max_blocks > 0) capacity = std::min<int64_t>(capacity, p->max_blocks);
   for (int l = 0; l < p->n_lanes; ++l) {
     rv_plan::Lane &lane = p->lanes[l];
     int64_t share = all_elems > 0 ? capacity * lane.elems / all_elems : 0;
@@ -1359,6 +1361,13 @@ int rv_plan_read_trace(rv_plan *p, int lane, uint64_t *out4) {
   DeviceGuard g(p->device);
   RV_CUDA(cudaDeviceSynchronize());
   RV_CUDA(cudaMemcpy(out4, p->trace + 4 * lane, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return RV_OK;
+}
+
+int rv_plan_set_max_blocks(rv_plan *p, int max_blocks) {
+  if (!p || max_blocks < 0) return set_err(RV_E_ARG, "bad block budget");
+  p->max_blocks = max_blocks;
+  p->dirty = true;
   return RV_OK;
 }
 

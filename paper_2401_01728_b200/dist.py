@@ -86,7 +86,8 @@ class DistRingGroup:
 
     def __init__(self, schedule=None, src=None, dst=None, *, starts: Sequence[int] | None = None,
                  lens: Sequence[int] | None = None, cluster_id: int | None = None, acc: str = "f64",
-                 lanes: int = 1, group=None, timeout_s: float | None = None, protocol: str = "auto"):
+                 lanes: int = 1, group=None, timeout_s: float | None = None, protocol: str = "auto",
+                 max_blocks: int = 0):
         import torch.distributed as dist
 
         if src is None:
@@ -125,6 +126,8 @@ class DistRingGroup:
             self.plan.set_lanes(lanes)
         if timeout_s is not None:
             self.plan.set_timeout(timeout_s)
+        if max_blocks:
+            self.plan.set_max_blocks(max_blocks)
         protocol = choose_protocol(protocol, total * src.element_size())
         self.protocol = protocol
         self.plan.set_protocol(protocol)

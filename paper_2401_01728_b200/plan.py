@@ -88,6 +88,9 @@ class DevicePlan:
     def set_push_peers(self, areas: Sequence[int]) -> None:
         N.check(self.lib.rv_plan_set_push_peers(self._h, N.ptr_array(areas)), "rv_plan_set_push_peers")
 
+    def set_max_blocks(self, n: int) -> None:
+        N.check(self.lib.rv_plan_set_max_blocks(self._h, int(n)), "rv_plan_set_max_blocks")
+
     def set_trace(self, enable: bool = True) -> None:
         N.check(self.lib.rv_plan_set_trace(self._h, int(bool(enable))), "rv_plan_set_trace")
 

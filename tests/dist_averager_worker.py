@@ -38,13 +38,16 @@ def main():
         init = [torch.randn(n, device=dev, generator=torch.Generator(device=dev).manual_seed(7 + m))
                 for m in range(world)]
         live = init[rank].clone()
-        avg = AsyncAverager(live, starts=starts, lens=lens, kappa=kappa, tau=tau, protocol=proto, graph=graph)
+        avg = AsyncAverager(live, starts=starts, lens=lens, kappa=kappa, tau=tau, protocol=proto, graph=graph,
+                            sm_budget=(8 if graph else 0))
         shadow = [x.clone() for x in init]
         snap = None
         pending = None
         steps = 4 * kappa + tau + 1
         for t in range(1, steps + 1):
-            live.sub_(grad(rank, t, n, dev), alpha=eta)
+            g_t = grad(rank, t, n, dev)
+            avg.before_update()
+            live.sub_(g_t, alpha=eta)
             avg.step()
             for m in range(world):
                 shadow[m].sub_(grad(m, t, n, dev), alpha=eta)
