@@ -57,11 +57,15 @@ def main():
             order = sorted(range(world), key=lambda r: (world - 1 - r) if reverse_ids else r)
             vals = [xs[r] for r in order]  # ascending cluster id
             want = ring_oracle.ring_mean(starts, lens, vals, acc=acc)[order.index(rank)].astype(npdt)
-            off = 1 if src_ne_dst else 0
-            buf = torch.empty(total + off + 4, dtype=dt, device=f"cuda:{local}")
+            off = 8 + (1 if src_ne_dst else 0)
+            buf = torch.full((total + off + 8,), -1234.5, dtype=dt, device=f"cuda:{local}")  # guard bands
             x = buf[off:off + total]
             x.copy_(torch.from_numpy(xs[rank]))
-            dst = torch.full((total,), float("nan"), dtype=dt, device=f"cuda:{local}") if src_ne_dst else None
+            dbuf = torch.full((total + 16,), -1234.5, dtype=dt, device=f"cuda:{local}") if src_ne_dst else None
+            dst = None
+            if src_ne_dst:
+                dst = dbuf[8:8 + total]
+                dst.fill_(float("nan"))
             g = DistRingGroup(src=x, dst=dst, starts=starts, lens=lens, cluster_id=cid, acc=acc, lanes=lanes,
                               protocol=proto)
             streams = [torch.cuda.Stream() for _ in range(lanes)]
@@ -70,6 +74,14 @@ def main():
             g.average(streams)
             torch.cuda.synchronize()
             g.check()
+            hb = buf.cpu().numpy()
+            guards_ok = (hb[:off] == -1234.5).all() and (hb[off + total:] == -1234.5).all()
+            if dbuf is not None:
+                hd = dbuf.cpu().numpy()
+                guards_ok = guards_ok and (hd[:8] == -1234.5).all() and (hd[8 + total:] == -1234.5).all()
+            if not guards_ok:
+                print(f"rank {rank} case {ci} {proto}: write outside the member vector", flush=True)
+                failures += 1
             got = (dst if dst is not None else x).cpu().numpy()
             if not np.array_equal(bits(got), bits(want)):
                 bad = int(np.sum(bits(got) != bits(want)))

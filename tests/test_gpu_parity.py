@@ -40,18 +40,28 @@ def make_sched(lens, c):
     return RingSchedule(tuple(rings), start)
 
 
+GUARD = 5  # sentinel elements on both sides of every member vector
+
+
 def run_inplace(sched, rows, dtype, acc="f64", device=0, offsets=None):
     """Copy rows to device (optionally at element offsets inside larger
-    buffers), average in place, return host arrays."""
-    ts, views = {}, []
+    buffers), average in place, return host arrays.  Every buffer carries
+    sentinel guard bands around the member vector; a write outside
+    [0, total) fails the test (compute-sanitizer is closed on this pool)."""
+    ts, views, bufs = {}, [], []
+    sentinel = -1234.5
     for m, r in enumerate(rows):
-        off = 0 if offsets is None else offsets[m]
-        buf = torch.empty(len(r) + off + 3, dtype=dtype, device=f"cuda:{device}")
+        off = GUARD + (0 if offsets is None else offsets[m])
+        buf = torch.full((len(r) + off + GUARD,), sentinel, dtype=dtype, device=f"cuda:{device}")
         v = buf[off:off + len(r)]
         v.copy_(torch.from_numpy(np.ascontiguousarray(r)))
         ts[m] = v
         views.append(v)
+        bufs.append((buf, off, len(r)))
     rv.ring_mean_(sched, ts, acc=acc)
+    for buf, off, n in bufs:
+        host = buf.cpu().numpy()
+        assert (host[:off] == sentinel).all() and (host[off + n:] == sentinel).all(), "write outside the vector"
     return np.stack([v.cpu().numpy() for v in views])
 
 
