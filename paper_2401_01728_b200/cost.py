@@ -12,8 +12,9 @@ with alpha the fixed cost (launch + arrive/depart barriers) and beta the
 sustained per-GPU, per-direction NVLink rate of the transport.  ``fit``
 calibrates (alpha, beta) by least squares on relative error from sweep rows
 (tools/sweep.py output); ``CALIBRATED`` holds the values fitted on
-profiles/r01/sweep_n4.jsonl (4 x B200, 24 shard-size x ring-count points,
-max relative error 3.2 % for pull).
+profiles/r01/sweep_n4_current.jsonl (4 x B200, 24 shard-size x ring-count
+points from 1 MiB to 8 GiB per cluster; max relative error 10 % for pull,
+13.5 % for push, under 3 % above 32 MiB per cluster).
 """
 
 from __future__ import annotations
@@ -34,8 +35,8 @@ class NvlinkModel:
 
 
 CALIBRATED = {
-    "pull": NvlinkModel(26.48e-6, 645.1e9, "profiles/r01/sweep_n4.jsonl (4 GPUs)"),
-    "push": NvlinkModel(56.32e-6, 719.3e9, "profiles/r01/sweep_n4.jsonl (4 GPUs, fixed 256 KB units)"),
+    "pull": NvlinkModel(27.89e-6, 644.6e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs)"),
+    "push": NvlinkModel(31.97e-6, 682.4e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs, adaptive units)"),
     "nccl": NvlinkModel(3.16e-6, 606.2e9, "profiles/r01/sweep_n4.jsonl; + 23.3 us per ring call"),
 }
 

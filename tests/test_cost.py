@@ -10,7 +10,7 @@ import paper_2401_01728_b200 as rv
 from paper_2401_01728_b200 import cli, cost
 from conftest import ROOT, GOLDEN
 
-SWEEP = os.path.join(ROOT, "profiles", "r01", "sweep_n4.jsonl")
+SWEEP = os.path.join(ROOT, "profiles", "r01", "sweep_n4_current.jsonl")
 
 
 def rows():
@@ -18,11 +18,14 @@ def rows():
         return [json.loads(l) for l in f if l.strip()]
 
 
-def test_pull_model_fits_measured_sweep():
-    model, err = cost.fit(rows(), "pull")
-    assert err < 0.05
-    assert 600e9 < model.beta_Bps < 700e9
-    assert abs(model.beta_Bps - cost.CALIBRATED["pull"].beta_Bps) / model.beta_Bps < 0.01
+def test_models_fit_measured_sweep():
+    for proto, tol in (("pull", 0.11), ("push", 0.14)):
+        model, err = cost.fit(rows(), proto)
+        assert err < tol, proto
+        assert 600e9 < model.beta_Bps < 720e9
+        assert abs(model.beta_Bps - cost.CALIBRATED[proto].beta_Bps) / model.beta_Bps < 0.01
+        big = [r for r in rows() if r["bytes_per_cluster"] >= 32 << 20]
+        assert cost.fit(big, proto)[1] < 0.04
 
 
 def test_model_shape_and_reference_contrast():

@@ -311,3 +311,23 @@ def test_device_checkpoint_roundtrip(tmp_path):
     formats.save_device_checkpoint(tmp_path / "m.ckpt", t)
     back = formats.read_checkpoint(tmp_path / "m.ckpt")
     assert np.array_equal(back, t.double().cpu().numpy())
+
+
+@pytest.mark.multigpu
+def test_local_group_several_clusters_per_device():
+    # 4 clusters on 2 GPUs (2 per GPU) in one process: each device folds the
+    # chunks of its own positions, the two devices meet through flags
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    c = 4
+    lens = [300007, 11, 4096, 77777]
+    sched = make_sched(lens, c)
+    rng = np.random.Generator(np.random.Philox(key=44))
+    rows = [rng.normal(0, 1, sched.total_params).astype(np.float32) for _ in range(c)]
+    want = np.stack(ring_oracle.ring_mean([r.start for r in sched.rings], lens, rows)).astype(np.float32)
+    for placement in ([0, 0, 1, 1], [0, 1, 0, 1], [1, 0, 0, 0]):
+        ts = {m: torch.from_numpy(rows[m]).to(f"cuda:{placement[m]}") for m in range(c)}
+        rv.ring_mean_(sched, ts)
+        got = np.stack([ts[m].cpu().numpy() for m in range(c)])
+        assert bits_equal(got, want), placement
