@@ -34,761 +34,10 @@
 
 namespace {
 
-// ---------------------------------------------------------------------------
-// error plumbing
-
-thread_local std::string g_err;
-
-int set_err(int code, const char *fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof(buf), fmt, ap);
-  va_end(ap);
-  g_err = buf;
-  return code;
-}
-
-#define RV_CUDA(call)                                                              \
-  do {                                                                             \
-    cudaError_t e_ = (call);                                                       \
-    if (e_ != cudaSuccess)                                                         \
-      return set_err(RV_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));   \
-  } while (0)
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
-
-// ---------------------------------------------------------------------------
-// device-side types
-
-constexpr int kThreads = 256;
-constexpr unsigned kStatusTimeout = 1u;
-constexpr int64_t kUnitBytes = 256 * 1024;    // push protocol: largest flagged unit
-constexpr int64_t kMinUnitBytes = 16 * 1024;  // push protocol: smallest flagged unit
-
-struct Seg {
-  int64_t lo, hi;            // chunk [lo, hi) in elements
-  int64_t body_lo, body_hi;  // 16-byte aligned vector body inside it
-  int64_t stage_off;         // push: element offset of this chunk in the owner's staging slot
-  int64_t unit0;             // push: first unit index of this chunk (per owner, per lane)
-  int32_t k;                 // fold start position = owner position (chunk index in its ring)
-  int32_t ring;
-};
-
-struct LaneState {
-  unsigned long long epoch;     // cycles completed on this lane
-  unsigned long long signaled;  // last epoch whose arrive flags were posted
-  unsigned int done;            // blocks finished in the running cycle
-  unsigned int pad;
-};
-
-struct CycleParams {
-  const void *src[RV_MAX_CLUSTERS];
-  void *dst[RV_MAX_CLUSTERS];
-  void *stage[RV_MAX_CLUSTERS];                 // push: owner q's staging area (as mapped here)
-  unsigned long long *pflags[RV_MAX_CLUSTERS];  // push: owner q's unit flags (as mapped here)
-  unsigned long long *peer_flags[RV_MAX_RANKS]; // rank r's barrier flag area (as mapped here)
-  const Seg *segs;             // pull: this device's chunks; push: every owner's, owner-major
-  const int64_t *tile_prefix;  // pull: nseg + 1 entries
-  unsigned long long *my_flags;
-  LaneState *state;
-  unsigned int *status;        // [0] code, [1] diag
-  unsigned long long *trace;   // optional: [start, ready, work done, departed] (globaltimer ns)
-  int64_t n_tiles;             // pull
-  int64_t stride;              // push: staging elements per writer slot
-  int64_t units_max;           // push: unit-flag slots per (lane, writer)
-  int64_t scatter_umax;        // push: max units over the other owners
-  int64_t unit_vecs;           // push: vectors per unit
-  int64_t ounits[RV_MAX_CLUSTERS];
-  int oseg_base[RV_MAX_CLUSTERS + 1];
-  unsigned long long timeout_ns;
-  double inv_c;
-  int C, nseg, rank, n_ranks, lane, pow2, me;
-};
-
-// flag slot of (lane, sender rank, phase) inside a receiver's barrier area
-__host__ __device__ inline size_t flag_index(int lane, int sender, int phase) {
-  return ((size_t)lane * RV_MAX_RANKS + (size_t)sender) * 2 + (size_t)phase;
-}
-
-// push: flag slot of (lane, writer, unit) inside an owner's unit-flag area
-__host__ __device__ inline size_t pflag_index(int lane, int c, int writer, int64_t units_max, int64_t u) {
-  return ((size_t)lane * c + (size_t)writer) * (size_t)units_max + (size_t)u;
-}
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Spin until *f >= e.  Returns false on timeout (status set, diag recorded)
-// or when another block already failed.
-__device__ bool wait_flag(const CycleParams &p, const unsigned long long *f, unsigned long long e,
-                          unsigned long long t0, unsigned diag) {
-  unsigned spins = 0;
-  while (ld_acquire_sys(f) < e) {
-    if ((++spins & 255u) == 0) {
-      if (*(volatile unsigned *)p.status != 0) return false;
-      if (globaltimer() - t0 > p.timeout_ns) {
-        if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u) p.status[1] = diag;
-        return false;
-      }
-    }
-  }
-  return true;
-}
-
-// Wait until every peer posted `phase` for epoch e.
-__device__ bool wait_peers(const CycleParams &p, int phase, unsigned long long e) {
-  const unsigned long long t0 = globaltimer();
-  for (int r = 0; r < p.n_ranks; ++r) {
-    if (r == p.rank) continue;
-    const unsigned diag = ((unsigned)phase << 16) | ((unsigned)p.lane << 8) | (unsigned)r;
-    if (!wait_flag(p, p.my_flags + flag_index(p.lane, r, phase), e, t0, diag)) return false;
-  }
-  return true;
-}
-
-__device__ void post_peers(const CycleParams &p, int phase, unsigned long long e) {
-  for (int r = 0; r < p.n_ranks; ++r) {
-    if (r == p.rank) continue;
-    st_release_sys(p.peer_flags[r] + flag_index(p.lane, p.rank, phase), e);
-  }
-}
-
-// Optional phase trace (thread 0 of each block): earliest start, latest
-// "ready for data" (pull: arrive barrier passed), latest end of data work,
-// and the moment the depart barrier completed.
-__device__ __forceinline__ void trace_min(const CycleParams &p, int slot) {
-  if (p.trace) atomicMin(p.trace + slot, globaltimer());
-}
-__device__ __forceinline__ void trace_max(const CycleParams &p, int slot) {
-  if (p.trace) atomicMax(p.trace + slot, globaltimer());
-}
-
-// Exit barrier: the last block of this launch tells every peer that all of
-// this device's stores (local and remote) are done, then waits for theirs,
-// so nobody resumes training on a buffer a peer is still writing.
-__device__ void depart(const CycleParams &p, unsigned long long epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    trace_max(p, 2);
-    __threadfence_system();
-    const unsigned prev = atomicAdd(&p.state->done, 1u);
-    if (prev == gridDim.x - 1) {
-      __threadfence_system();
-      post_peers(p, 1, epoch);
-      if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
-      trace_max(p, 3);
-      p.state->done = 0u;
-      *(volatile unsigned long long *)&p.state->epoch = epoch;
-      __threadfence();
-    }
-  }
-}
-
-template <int VB>
-struct RawVec;
-template <>
-struct RawVec<16> {
-  using type = uint4;
-};
-template <>
-struct RawVec<8> {
-  using type = uint2;
-};
-template <>
-struct RawVec<4> {
-  using type = unsigned int;
-};
-
-template <typename T, int VB>
-union Lanes {
-  typename RawVec<VB>::type raw;
-  T v[VB / sizeof(T)];
-};
-
-template <typename T, typename Acc>
-__device__ __forceinline__ T finish(Acc acc, const CycleParams &p) {
-  // IEEE true division by C (multiring.py:219).  For C a power of two the
-  // product with the exact reciprocal is the same correctly rounded value.
-  const Acc q = p.pow2 ? acc * (Acc)p.inv_c : acc / (Acc)p.C;
-  return (T)q;
-}
-
-// Element i of member m as this device reads it.  Pull: the member's own
-// buffer (local or peer).  Push: the owner's own buffer for m == me, else the
-// staging slot member m pushed into.
-template <typename T, bool PUSH>
-__device__ __forceinline__ const T *member_elem(const CycleParams &p, const Seg &s, int m, int64_t i) {
-  if (!PUSH || m == p.me) return static_cast<const T *>(p.src[m]) + i;
-  return static_cast<const T *>(p.stage[p.me]) + ((int64_t)m * p.stride + s.stage_off + (i - s.lo));
-}
-
-// Fold of one element (chunk edges, misaligned buffers): ring order from s.k.
-template <typename T, typename Acc, bool PUSH>
-__device__ __forceinline__ void fold_scalar(const CycleParams &p, const Seg &s, int64_t i) {
-  int m = s.k;
-  Acc acc = (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
-  for (int q = 1; q < p.C; ++q) {
-    m = (m + 1 == p.C) ? 0 : m + 1;
-    acc = acc + (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
-  }
-  const T out = finish<T, Acc>(acc, p);
-  for (int q = 0; q < p.C; ++q) __stcs(static_cast<T *>(p.dst[q]) + i, out);
-}
-
-// Fold one pass of chunk s: this thread takes vectors j0 + u*kThreads
-// (u < U, below jend), loads all C members of each (U*C loads in flight),
-// folds in ring order, divides, and stores the mean into all C buffers.
-template <typename T, typename Acc, int CB, int VB, int U, bool PUSH>
-__device__ __forceinline__ void fold_pass(const CycleParams &p, const Seg &s, int64_t j0, int64_t jend) {
-  constexpr int N = VB / sizeof(T);
-  using Raw = typename RawVec<VB>::type;
-  Lanes<T, VB> x[U][CB];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t j = j0 + (int64_t)u * kThreads;
-    if (j < jend) {
-      const int64_t i = s.body_lo + j * N;
-#pragma unroll
-      for (int q = 0; q < CB; ++q) {
-        if (q < p.C) {
-          int m = s.k + q;
-          if (m >= p.C) m -= p.C;
-          x[u][q].raw = __ldcs(reinterpret_cast<const Raw *>(member_elem<T, PUSH>(p, s, m, i)));
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t j = j0 + (int64_t)u * kThreads;
-    if (j < jend) {
-      Lanes<T, VB> out;
-#pragma unroll
-      for (int e = 0; e < N; ++e) {
-        Acc acc = (Acc)x[u][0].v[e];
-#pragma unroll
-        for (int q = 1; q < CB; ++q)
-          if (q < p.C) acc = acc + (Acc)x[u][q].v[e];
-        out.v[e] = finish<T, Acc>(acc, p);
-      }
-      const int64_t i = s.body_lo + j * N;
-#pragma unroll
-      for (int q = 0; q < CB; ++q)
-        if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// pull protocol: the owner of chunk k reads chunk k of every member (local
-// HBM or NVLink peer loads) and pushes the mean into every member.  Arrive
-// barrier first (peers' inputs final), depart barrier last.
-
-// Two 256-thread blocks per SM (<= 128 registers): measured 1.18 ms vs
-// 1.47 ms at one block per SM on the co-resident BERT cycle.
-template <typename T, typename Acc, int CB, int VB, int U, int MINB = 2>
-__global__ void __launch_bounds__(kThreads, MINB)
-ring_cycle_kernel(const __grid_constant__ CycleParams p) {
-  constexpr int N = VB / sizeof(T);
-  __shared__ int s_go;
-  unsigned long long epoch = 0;
-
-  if (threadIdx.x == 0) trace_min(p, 0);
-  if (p.n_ranks > 1) {
-    if (threadIdx.x == 0) {
-      epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
-      int go = (*(volatile unsigned *)p.status == 0);
-      if (go) {
-        // first block of this launch posts "inputs final" to every peer
-        if (atomicCAS(&p.state->signaled, epoch - 1ull, epoch) == epoch - 1ull) {
-          __threadfence_system();
-          post_peers(p, 0, epoch);
-        }
-        go = wait_peers(p, 0, epoch);
-      }
-      trace_max(p, 1);
-      s_go = go;
-    }
-    __syncthreads();
-  } else {
-    if (threadIdx.x == 0) s_go = 1;
-    __syncthreads();
-  }
-
-  if (s_go) {
-    const int64_t tile_vecs = (int64_t)kThreads * U;
-    for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-      int a = 0, b = p.nseg - 1;
-      while (a < b) {
-        const int mid = (a + b + 1) >> 1;
-        if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
-      }
-      const Seg s = p.segs[a];
-      const int64_t local_tile = t - __ldg(p.tile_prefix + a);
-      const int64_t nvec = (s.body_hi - s.body_lo) / N;
-      const int64_t jbeg = local_tile * tile_vecs;
-      fold_pass<T, Acc, CB, VB, U, false>(p, s, jbeg + threadIdx.x, min(nvec, jbeg + tile_vecs));
-      if (local_tile == 0) {
-        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
-        if ((int64_t)threadIdx.x < nhead + ntail) {
-          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
-                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
-          fold_scalar<T, Acc, false>(p, s, i);
-        }
-      }
-    }
-  }
-  if (p.n_ranks > 1) {
-    depart(p, epoch);
-  } else if (p.trace) {
-    __syncthreads();
-    if (threadIdx.x == 0) trace_max(p, 2);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// push protocol (one position per rank, rank == position): NVLink carries
-// stores only.  Scatter: this rank copies its chunk-q slice of every ring into
-// owner q's staging slot and raises one release flag per 256 KB unit.  Fold:
-// for its own chunk, once every writer's flag for a unit is up, the owner
-// folds its own values and the staged ones in ring order and pushes the mean
-// into all members.  No arrive barrier is needed: a member's chunk reaches
-// the owner only after its kernel started (inputs final), and the owner
-// writes a member's buffer only after receiving that member's data for the
-// same unit.  The depart barrier still closes the cycle.
-
-template <typename T>
-__device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
-  int a = 0, b = nseg - 1;
-  while (a < b) {
-    const int mid = (a + b + 1) >> 1;
-    if (segs[mid].unit0 <= u) a = mid; else b = mid - 1;
-  }
-  return segs[a];
-}
-
-template <typename T, typename Acc, int CB, int VB, int U>
-__global__ void __launch_bounds__(kThreads, 2)
-ring_push_kernel(const __grid_constant__ CycleParams p) {
-  constexpr int N = VB / sizeof(T);
-  constexpr int KC = (U * CB) < 8 ? (U * CB) : 8;  // vectors in flight per thread when copying
-  using Raw = typename RawVec<VB>::type;
-  __shared__ int s_ok;
-  __shared__ unsigned long long s_epoch;
-  if (threadIdx.x == 0) {
-    trace_min(p, 0);
-    trace_max(p, 1);
-    s_epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
-    s_ok = (*(volatile unsigned *)p.status == 0);
-  }
-  __syncthreads();
-  const unsigned long long epoch = s_epoch;
-  const int C = p.C, me = p.me;
-  const int64_t n_scatter = (int64_t)(C - 1) * p.scatter_umax;
-  const int64_t n_work = n_scatter + p.ounits[me];
-  const unsigned long long t0 = globaltimer();
-
-  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
-    if (!s_ok) break;
-    if (w < n_scatter) {
-      const int r = (int)(w % (C - 1));
-      const int64_t u = w / (C - 1);
-      int q = me + 1 + r;
-      if (q >= C) q -= C;
-      if (u >= p.ounits[q]) continue;
-      const Seg s = find_unit<T>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
-      const int64_t uu = u - s.unit0;
-      const int64_t nvec = (s.body_hi - s.body_lo) / N;
-      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
-      const T *src = static_cast<const T *>(p.src[me]);
-      T *stg = static_cast<T *>(p.stage[q]) + ((int64_t)me * p.stride + s.stage_off - s.lo);
-      for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * KC) {
-        Raw v[KC];
-#pragma unroll
-        for (int c = 0; c < KC; ++c) {
-          const int64_t j = j0 + (int64_t)c * kThreads;
-          if (j < jend) v[c] = __ldcs(reinterpret_cast<const Raw *>(src + s.body_lo + j * N));
-        }
-#pragma unroll
-        for (int c = 0; c < KC; ++c) {
-          const int64_t j = j0 + (int64_t)c * kThreads;
-          if (j < jend) __stcs(reinterpret_cast<Raw *>(stg + s.body_lo + j * N), v[c]);
-        }
-      }
-      if (uu == 0) {
-        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
-        if ((int64_t)threadIdx.x < nhead + ntail) {
-          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
-                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
-          stg[i] = src[i];
-        }
-      }
-      __threadfence_system();  // this thread's stores, before the unit flag
-      __syncthreads();
-      if (threadIdx.x == 0)
-        st_release_sys(p.pflags[q] + pflag_index(p.lane, C, me, p.units_max, u), epoch);
-    } else {
-      const int64_t u = w - n_scatter;
-      const Seg s = find_unit<T>(p.segs + p.oseg_base[me], p.oseg_base[me + 1] - p.oseg_base[me], u);
-      if (threadIdx.x == 0) {
-        for (int m = 0; m < C && s_ok; ++m) {
-          if (m == me) continue;
-          const unsigned diag = (2u << 16) | ((unsigned)p.lane << 8) | (unsigned)m;
-          if (!wait_flag(p, p.pflags[me] + pflag_index(p.lane, C, m, p.units_max, u), epoch, t0, diag)) s_ok = 0;
-        }
-      }
-      __syncthreads();
-      if (!s_ok) break;
-      const int64_t uu = u - s.unit0;
-      const int64_t nvec = (s.body_hi - s.body_lo) / N;
-      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
-      for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * U)
-        fold_pass<T, Acc, CB, VB, U, true>(p, s, j0, jend);
-      if (uu == 0) {
-        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
-        if ((int64_t)threadIdx.x < nhead + ntail) {
-          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
-                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
-          fold_scalar<T, Acc, true>(p, s, i);
-        }
-      }
-      __syncthreads();  // s_ok is re-armed by thread 0 for the next unit
-    }
-  }
-  depart(p, epoch);
-}
-
-// ---------------------------------------------------------------------------
-// co-resident TMA path (all C members on this device, 16-byte congruent
-// buffers): HBM-bound, so tiles stream through shared memory with bulk async
-// copies.  Warp 0 / lane 0 produces: for each tile it loads the tile of all C
-// members (cp.async.bulk global->shared, completion on a per-stage mbarrier)
-// into a STAGES-deep ring.  Warps 1..8 consume: fold from shared memory in
-// ring order, write the mean tile to shared memory, and one consumer issues
-// C bulk stores (shared->global) of it, double-buffered.  No register
-// staging of loads, so each SM keeps STAGES * C * TV * 16 bytes in flight.
-
-constexpr int kTmaConsumers = 256;
-
-__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-  unsigned ok = 0;
-  while (!ok)
-    asm volatile(
-        "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
-        : "=r"(ok)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void *smem, const void *gmem, unsigned bytes, unsigned long long *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(smem)),
-               "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)),
-               "r"(bytes)
-               : "memory");
-}
-
-template <typename T, typename Acc, int CB, int TV, int STAGES>
-__global__ void __launch_bounds__(kTmaConsumers + 32, 2)
-ring_tma_kernel(const __grid_constant__ CycleParams p) {
-  constexpr int N = 16 / sizeof(T);
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][CB][TV]
-  uint4 *out = in + (size_t)STAGES * CB * TV;                          // [2][TV]
-  __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
-  const int tid = threadIdx.x;
-  const int C = p.C;
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    trace_min(p, 0);
-    trace_max(p, 1);
-  }
-  __syncthreads();
-
-  // the tiles this block owns: t = blockIdx.x + i * gridDim.x
-  auto seg_of = [&](int64_t t, int64_t *local) -> Seg {
-    int a = 0, b = p.nseg - 1;
-    while (a < b) {
-      const int mid = (a + b + 1) >> 1;
-      if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
-    }
-    *local = t - __ldg(p.tile_prefix + a);
-    return p.segs[a];
-  };
-
-  if (tid < 32) {
-    if (tid == 0) {  // producer
-      int stage = 0;
-      unsigned phase = 0;
-      int64_t n = 0;
-      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++n) {
-        int64_t lt;
-        const Seg s = seg_of(t, &lt);
-        const int64_t nvec = (s.body_hi - s.body_lo) / N;
-        const int64_t j0 = lt * TV;
-        const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
-        if (n >= STAGES) mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], (unsigned)(cnt * 16 * C));
-        if (cnt > 0) {
-          for (int q = 0; q < C; ++q) {
-            int m = s.k + q;
-            if (m >= C) m -= C;
-            bulk_load(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
-                      (unsigned)(cnt * 16), &full[stage]);
-          }
-        }
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-    return;
-  }
-
-  // consumers (256 threads)
-  const int c = tid - 32;
-  int stage = 0;
-  unsigned phase = 0;
-  int ob = 0;
-  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-    int64_t lt;
-    const Seg s = seg_of(t, &lt);
-    const int64_t nvec = (s.body_hi - s.body_lo) / N;
-    const int64_t j0 = lt * TV;
-    const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
-    mbar_wait(&full[stage], phase);
-    // consumer 0 finished the previous tile's store bookkeeping (out[ob] free)
-    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
-    for (int v = c; v < cnt; v += kTmaConsumers) {
-      Lanes<T, 16> x, o;
-      Acc acc[N];
-      x.raw = in[((size_t)stage * CB + 0) * TV + v];
-#pragma unroll
-      for (int e = 0; e < N; ++e) acc[e] = (Acc)x.v[e];
-#pragma unroll
-      for (int q = 1; q < CB; ++q) {
-        if (q < C) {
-          x.raw = in[((size_t)stage * CB + q) * TV + v];
-#pragma unroll
-          for (int e = 0; e < N; ++e) acc[e] = acc[e] + (Acc)x.v[e];
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < N; ++e) o.v[e] = finish<T, Acc>(acc[e], p);
-      out[ob * TV + v] = o.raw;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
-    if (c == 0) {
-      mbar_arrive(&empty[stage]);  // every consumer has read this stage
-      if (cnt > 0) {
-        for (int q = 0; q < C; ++q)
-          bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16));
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // out[ob ^ 1] reusable
-    }
-    if (lt == 0) {
-      const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
-      if ((int64_t)c < nhead + ntail) {
-        const int64_t i = (int64_t)c < nhead ? s.lo + c : s.body_hi + ((int64_t)c - nhead);
-        fold_scalar<T, Acc, false>(p, s, i);
-      }
-    }
-    ob ^= 1;
-    if (++stage == STAGES) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
-  if (c == 0) {
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    trace_max(p, 2);
-  }
-}
-
-// live <- mean + (live - snap); exactly mean where live == snap bitwise.
-template <typename T, typename U>
-__global__ void __launch_bounds__(kThreads)
-blend_kernel(T *__restrict__ live, const T *__restrict__ snap, const T *__restrict__ mean, int64_t n) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const T l = live[i], s = snap[i], m = __ldcs(mean + i);
-    U lb, sb;
-    memcpy(&lb, &l, sizeof(T));
-    memcpy(&sb, &s, sizeof(T));
-    live[i] = (lb == sb) ? m : (m + (l - s));
-  }
-}
-
-template <typename T, typename U>
-__global__ void __launch_bounds__(kThreads)
-blend_kernel_v4(T *__restrict__ live, const T *__restrict__ snap, const T *__restrict__ mean, int64_t nvec) {
-  constexpr int N = 16 / sizeof(T);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nvec; j += stride) {
-    Lanes<T, 16> l, s, m, o;
-    l.raw = *reinterpret_cast<const uint4 *>(live + j * N);
-    s.raw = __ldcs(reinterpret_cast<const uint4 *>(snap + j * N));
-    m.raw = __ldcs(reinterpret_cast<const uint4 *>(mean + j * N));
-#pragma unroll
-    for (int e = 0; e < N; ++e) {
-      U lb, sb;
-      memcpy(&lb, &l.v[e], sizeof(T));
-      memcpy(&sb, &s.v[e], sizeof(T));
-      o.v[e] = (lb == sb) ? m.v[e] : (m.v[e] + (l.v[e] - s.v[e]));
-    }
-    *reinterpret_cast<uint4 *>(live + j * N) = o.raw;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// kernel dispatch
-
-using KernelFn = void (*)(CycleParams);
-
-enum Mode { kF32Acc64 = 0, kF32Native = 1, kF64 = 2 };
-
-// Vectors per thread per pass: U*C 16-byte loads in flight, kept within the
-// 128-register budget (fp64 storage and the push kernel's staging addresses
-// take more registers, so they run at half U).
-template <typename T, typename Acc, int VB>
-KernelFn pick_cb(int c, bool push, int *u_out) {
-  constexpr bool wide = sizeof(T) == 8;
-  if (push) {
-    if (c <= 2) { *u_out = 4; return ring_push_kernel<T, Acc, 2, VB, 4>; }
-    if (c <= 4) { *u_out = 2; return ring_push_kernel<T, Acc, 4, VB, 2>; }
-    if (c <= 8) { *u_out = 1; return ring_push_kernel<T, Acc, 8, VB, 1>; }
-    *u_out = 1;
-    return ring_push_kernel<T, Acc, 16, VB, 1>;
-  }
-  if constexpr (wide) {
-    if (c <= 2) { *u_out = 4; return ring_cycle_kernel<T, Acc, 2, VB, 4>; }
-    if (c <= 4) { *u_out = 2; return ring_cycle_kernel<T, Acc, 4, VB, 2>; }
-    if (c <= 8) { *u_out = 1; return ring_cycle_kernel<T, Acc, 8, VB, 1>; }
-  } else {
-    if (c <= 2) { *u_out = 8; return ring_cycle_kernel<T, Acc, 2, VB, 8>; }
-    if (c <= 4) { *u_out = 4; return ring_cycle_kernel<T, Acc, 4, VB, 4>; }
-    if (c <= 8) { *u_out = 2; return ring_cycle_kernel<T, Acc, 8, VB, 2>; }
-  }
-  *u_out = 1;
-  return ring_cycle_kernel<T, Acc, 16, VB, 1>;
-}
-
-// Tuning variants of the f32 / f64-fold vector pull kernel (RAVNEST_B200_VARIANT,
-// experiments only): 1 = half the vectors per thread, >= 3 blocks/SM;
-// 2 = half, >= 4 blocks/SM; 3 = same vectors, no register cap (1 block/SM).
-template <int CB, int U>
-KernelFn pick_variant(int v, int *u_out) {
-  constexpr int H = U > 1 ? U / 2 : 1;
-  switch (v) {
-    case 1: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 3>;
-    case 2: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 4>;
-    case 3: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 1>;
-    default: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 2>;
-  }
-}
-
-// Co-resident TMA kernel: 32 KB of member data per pipeline stage
-// (CB * TV * 16 bytes), 3 stages -> 104 KB of shared memory, two blocks per
-// SM (measured best of 3/4/6 stages: 0.918 of measured HBM on BERT C=8).
-constexpr int kTmaStages = 3;
-constexpr int kTmaStageBytes = 32 * 1024;
-
-template <typename T, typename Acc, int STAGES, int STAGE_BYTES>
-KernelFn pick_tma(int c, int *tv_out) {
-  if (c <= 2) { *tv_out = STAGE_BYTES / (2 * 16); return ring_tma_kernel<T, Acc, 2, STAGE_BYTES / (2 * 16), STAGES>; }
-  if (c <= 4) { *tv_out = STAGE_BYTES / (4 * 16); return ring_tma_kernel<T, Acc, 4, STAGE_BYTES / (4 * 16), STAGES>; }
-  if (c <= 8) { *tv_out = STAGE_BYTES / (8 * 16); return ring_tma_kernel<T, Acc, 8, STAGE_BYTES / (8 * 16), STAGES>; }
-  *tv_out = STAGE_BYTES / (16 * 16);
-  return ring_tma_kernel<T, Acc, 16, STAGE_BYTES / (16 * 16), STAGES>;
-}
-
-KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
-  // RAVNEST_B200_TMA_VARIANT (experiments): 1 = 6 stages, 2 = 4 stages (one
-  // block per SM), 3 = 8 stages of 16 KB
-  const char *ve = getenv("RAVNEST_B200_TMA_VARIANT");
-  const int v = ve ? atoi(ve) : 0;
-  int stages = kTmaStages;
-  KernelFn k;
-  if (v > 0 && mode == kF32Acc64) {
-    if (v == 1) { stages = 6; k = pick_tma<float, double, 6, kTmaStageBytes>(c, tv_out); }
-    else if (v == 2) { stages = 4; k = pick_tma<float, double, 4, kTmaStageBytes>(c, tv_out); }
-    else { stages = 8; k = pick_tma<float, double, 8, 16 * 1024>(c, tv_out); }
-  } else {
-    k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out)
-      : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes>(c, tv_out)
-                           : pick_tma<double, double, kTmaStages, kTmaStageBytes>(c, tv_out);
-  }
-  const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
-  *smem_out = (size_t)stages * cb * (*tv_out) * 16 + 2 * (size_t)(*tv_out) * 16;
-  return k;
-}
-
-KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
-  const char *ve = getenv("RAVNEST_B200_VARIANT");
-  const int variant = ve ? atoi(ve) : 0;
-  if (variant > 0 && mode == kF32Acc64 && vec && !push) {
-    if (c <= 2) return pick_variant<2, 8>(variant, u_out);
-    if (c <= 4) return pick_variant<4, 4>(variant, u_out);
-    if (c <= 8) return pick_variant<8, 2>(variant, u_out);
-    return pick_variant<16, 1>(variant, u_out);
-  }
-  switch (mode) {
-    case kF32Acc64: return vec ? pick_cb<float, double, 16>(c, push, u_out) : pick_cb<float, double, 4>(c, push, u_out);
-    case kF32Native: return vec ? pick_cb<float, float, 16>(c, push, u_out) : pick_cb<float, float, 4>(c, push, u_out);
-    default: return vec ? pick_cb<double, double, 16>(c, push, u_out) : pick_cb<double, double, 8>(c, push, u_out);
-  }
-}
+#include "rv_common.cuh"
+#include "rv_fold.cuh"
+#include "rv_kernels.cuh"
+#include "rv_dispatch.cuh"
 
 // ---------------------------------------------------------------------------
 // driver entry point for cuMemGetAddressRange (no link-time libcuda dependency)

@@ -1,0 +1,104 @@
+// Kernel selection: dtype / accumulation / member count / vector width /
+// transport -> template instantiation.
+// Part of the single translation unit ravnest_b200.cu (included inside its
+// anonymous namespace); see that file for the overview.
+#pragma once
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+
+using KernelFn = void (*)(CycleParams);
+
+enum Mode { kF32Acc64 = 0, kF32Native = 1, kF64 = 2 };
+
+// Vectors per thread per pass: U*C 16-byte loads in flight, kept within the
+// 128-register budget (fp64 storage and the push kernel's staging addresses
+// take more registers, so they run at half U).
+template <typename T, typename Acc, int VB>
+KernelFn pick_cb(int c, bool push, int *u_out) {
+  constexpr bool wide = sizeof(T) == 8;
+  if (push) {
+    if (c <= 2) { *u_out = 4; return ring_push_kernel<T, Acc, 2, VB, 4>; }
+    if (c <= 4) { *u_out = 2; return ring_push_kernel<T, Acc, 4, VB, 2>; }
+    if (c <= 8) { *u_out = 1; return ring_push_kernel<T, Acc, 8, VB, 1>; }
+    *u_out = 1;
+    return ring_push_kernel<T, Acc, 16, VB, 1>;
+  }
+  if constexpr (wide) {
+    if (c <= 2) { *u_out = 4; return ring_cycle_kernel<T, Acc, 2, VB, 4>; }
+    if (c <= 4) { *u_out = 2; return ring_cycle_kernel<T, Acc, 4, VB, 2>; }
+    if (c <= 8) { *u_out = 1; return ring_cycle_kernel<T, Acc, 8, VB, 1>; }
+  } else {
+    if (c <= 2) { *u_out = 8; return ring_cycle_kernel<T, Acc, 2, VB, 8>; }
+    if (c <= 4) { *u_out = 4; return ring_cycle_kernel<T, Acc, 4, VB, 4>; }
+    if (c <= 8) { *u_out = 2; return ring_cycle_kernel<T, Acc, 8, VB, 2>; }
+  }
+  *u_out = 1;
+  return ring_cycle_kernel<T, Acc, 16, VB, 1>;
+}
+
+// Tuning variants of the f32 / f64-fold vector pull kernel (RAVNEST_B200_VARIANT,
+// experiments only): 1 = half the vectors per thread, >= 3 blocks/SM;
+// 2 = half, >= 4 blocks/SM; 3 = same vectors, no register cap (1 block/SM).
+template <int CB, int U>
+KernelFn pick_variant(int v, int *u_out) {
+  constexpr int H = U > 1 ? U / 2 : 1;
+  switch (v) {
+    case 1: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 3>;
+    case 2: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 4>;
+    case 3: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 1>;
+    default: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 2>;
+  }
+}
+
+// Co-resident TMA kernel: 32 KB of member data per pipeline stage
+// (CB * TV * 16 bytes), 3 stages -> 104 KB of shared memory, two blocks per
+// SM (measured best of 3/4/6 stages: 0.918 of measured HBM on BERT C=8).
+constexpr int kTmaStages = 3;
+constexpr int kTmaStageBytes = 32 * 1024;
+
+template <typename T, typename Acc, int STAGES, int STAGE_BYTES>
+KernelFn pick_tma(int c, int *tv_out) {
+  if (c <= 2) { *tv_out = STAGE_BYTES / (2 * 16); return ring_tma_kernel<T, Acc, 2, STAGE_BYTES / (2 * 16), STAGES>; }
+  if (c <= 4) { *tv_out = STAGE_BYTES / (4 * 16); return ring_tma_kernel<T, Acc, 4, STAGE_BYTES / (4 * 16), STAGES>; }
+  if (c <= 8) { *tv_out = STAGE_BYTES / (8 * 16); return ring_tma_kernel<T, Acc, 8, STAGE_BYTES / (8 * 16), STAGES>; }
+  *tv_out = STAGE_BYTES / (16 * 16);
+  return ring_tma_kernel<T, Acc, 16, STAGE_BYTES / (16 * 16), STAGES>;
+}
+
+KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
+  // RAVNEST_B200_TMA_VARIANT (experiments): 1 = 6 stages, 2 = 4 stages (one
+  // block per SM), 3 = 8 stages of 16 KB
+  const char *ve = getenv("RAVNEST_B200_TMA_VARIANT");
+  const int v = ve ? atoi(ve) : 0;
+  int stages = kTmaStages;
+  KernelFn k;
+  if (v > 0 && mode == kF32Acc64) {
+    if (v == 1) { stages = 6; k = pick_tma<float, double, 6, kTmaStageBytes>(c, tv_out); }
+    else if (v == 2) { stages = 4; k = pick_tma<float, double, 4, kTmaStageBytes>(c, tv_out); }
+    else { stages = 8; k = pick_tma<float, double, 8, 16 * 1024>(c, tv_out); }
+  } else {
+    k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out)
+      : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes>(c, tv_out)
+                           : pick_tma<double, double, kTmaStages, kTmaStageBytes>(c, tv_out);
+  }
+  const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
+  *smem_out = (size_t)stages * cb * (*tv_out) * 16 + 2 * (size_t)(*tv_out) * 16;
+  return k;
+}
+
+KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
+  const char *ve = getenv("RAVNEST_B200_VARIANT");
+  const int variant = ve ? atoi(ve) : 0;
+  if (variant > 0 && mode == kF32Acc64 && vec && !push) {
+    if (c <= 2) return pick_variant<2, 8>(variant, u_out);
+    if (c <= 4) return pick_variant<4, 4>(variant, u_out);
+    if (c <= 8) return pick_variant<8, 2>(variant, u_out);
+    return pick_variant<16, 1>(variant, u_out);
+  }
+  switch (mode) {
+    case kF32Acc64: return vec ? pick_cb<float, double, 16>(c, push, u_out) : pick_cb<float, double, 4>(c, push, u_out);
+    case kF32Native: return vec ? pick_cb<float, float, 16>(c, push, u_out) : pick_cb<float, float, 4>(c, push, u_out);
+    default: return vec ? pick_cb<double, double, 16>(c, push, u_out) : pick_cb<double, double, 8>(c, push, u_out);
+  }
+}

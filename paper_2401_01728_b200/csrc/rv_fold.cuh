@@ -1,0 +1,100 @@
+// The ring-order fold: vector types, the IEEE divide by C, member addressing
+// for the pull and push transports, scalar and vector fold passes.
+// Part of the single translation unit ravnest_b200.cu (included inside its
+// anonymous namespace); see that file for the overview.
+#pragma once
+
+template <int VB>
+struct RawVec;
+template <>
+struct RawVec<16> {
+  using type = uint4;
+};
+template <>
+struct RawVec<8> {
+  using type = uint2;
+};
+template <>
+struct RawVec<4> {
+  using type = unsigned int;
+};
+
+template <typename T, int VB>
+union Lanes {
+  typename RawVec<VB>::type raw;
+  T v[VB / sizeof(T)];
+};
+
+template <typename T, typename Acc>
+__device__ __forceinline__ T finish(Acc acc, const CycleParams &p) {
+  // IEEE true division by C (multiring.py:219).  For C a power of two the
+  // product with the exact reciprocal is the same correctly rounded value.
+  const Acc q = p.pow2 ? acc * (Acc)p.inv_c : acc / (Acc)p.C;
+  return (T)q;
+}
+
+// Element i of member m as this device reads it.  Pull: the member's own
+// buffer (local or peer).  Push: the owner's own buffer for m == me, else the
+// staging slot member m pushed into.
+template <typename T, bool PUSH>
+__device__ __forceinline__ const T *member_elem(const CycleParams &p, const Seg &s, int m, int64_t i) {
+  if (!PUSH || m == p.me) return static_cast<const T *>(p.src[m]) + i;
+  return static_cast<const T *>(p.stage[p.me]) + ((int64_t)m * p.stride + s.stage_off + (i - s.lo));
+}
+
+// Fold of one element (chunk edges, misaligned buffers): ring order from s.k.
+template <typename T, typename Acc, bool PUSH>
+__device__ __forceinline__ void fold_scalar(const CycleParams &p, const Seg &s, int64_t i) {
+  int m = s.k;
+  Acc acc = (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
+  for (int q = 1; q < p.C; ++q) {
+    m = (m + 1 == p.C) ? 0 : m + 1;
+    acc = acc + (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
+  }
+  const T out = finish<T, Acc>(acc, p);
+  for (int q = 0; q < p.C; ++q) __stcs(static_cast<T *>(p.dst[q]) + i, out);
+}
+
+// Fold one pass of chunk s: this thread takes vectors j0 + u*kThreads
+// (u < U, below jend), loads all C members of each (U*C loads in flight),
+// folds in ring order, divides, and stores the mean into all C buffers.
+template <typename T, typename Acc, int CB, int VB, int U, bool PUSH>
+__device__ __forceinline__ void fold_pass(const CycleParams &p, const Seg &s, int64_t j0, int64_t jend) {
+  constexpr int N = VB / sizeof(T);
+  using Raw = typename RawVec<VB>::type;
+  Lanes<T, VB> x[U][CB];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = j0 + (int64_t)u * kThreads;
+    if (j < jend) {
+      const int64_t i = s.body_lo + j * N;
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        if (q < p.C) {
+          int m = s.k + q;
+          if (m >= p.C) m -= p.C;
+          x[u][q].raw = __ldcs(reinterpret_cast<const Raw *>(member_elem<T, PUSH>(p, s, m, i)));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t j = j0 + (int64_t)u * kThreads;
+    if (j < jend) {
+      Lanes<T, VB> out;
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        Acc acc = (Acc)x[u][0].v[e];
+#pragma unroll
+        for (int q = 1; q < CB; ++q)
+          if (q < p.C) acc = acc + (Acc)x[u][q].v[e];
+        out.v[e] = finish<T, Acc>(acc, p);
+      }
+      const int64_t i = s.body_lo + j * N;
+#pragma unroll
+      for (int q = 0; q < CB; ++q)
+        if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
+    }
+  }
+}

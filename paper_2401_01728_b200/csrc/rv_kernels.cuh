@@ -1,0 +1,392 @@
+// Kernels: pull/co-resident register path, push transport, co-resident TMA
+// path, delayed-update blend.
+// Part of the single translation unit ravnest_b200.cu (included inside its
+// anonymous namespace); see that file for the overview.
+#pragma once
+
+// ---------------------------------------------------------------------------
+// pull protocol: the owner of chunk k reads chunk k of every member (local
+// HBM or NVLink peer loads) and pushes the mean into every member.  Arrive
+// barrier first (peers' inputs final), depart barrier last.
+
+// Two 256-thread blocks per SM (<= 128 registers): measured 1.18 ms vs
+// 1.47 ms at one block per SM on the co-resident BERT cycle.
+template <typename T, typename Acc, int CB, int VB, int U, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB)
+ring_cycle_kernel(const __grid_constant__ CycleParams p) {
+  constexpr int N = VB / sizeof(T);
+  __shared__ int s_go;
+  unsigned long long epoch = 0;
+
+  if (threadIdx.x == 0) trace_min(p, 0);
+  if (p.n_ranks > 1) {
+    if (threadIdx.x == 0) {
+      epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
+      int go = (*(volatile unsigned *)p.status == 0);
+      if (go) {
+        // first block of this launch posts "inputs final" to every peer
+        if (atomicCAS(&p.state->signaled, epoch - 1ull, epoch) == epoch - 1ull) {
+          __threadfence_system();
+          post_peers(p, 0, epoch);
+        }
+        go = wait_peers(p, 0, epoch);
+      }
+      trace_max(p, 1);
+      s_go = go;
+    }
+    __syncthreads();
+  } else {
+    if (threadIdx.x == 0) s_go = 1;
+    __syncthreads();
+  }
+
+  if (s_go) {
+    const int64_t tile_vecs = (int64_t)kThreads * U;
+    for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+      int a = 0, b = p.nseg - 1;
+      while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
+      }
+      const Seg s = p.segs[a];
+      const int64_t local_tile = t - __ldg(p.tile_prefix + a);
+      const int64_t nvec = (s.body_hi - s.body_lo) / N;
+      const int64_t jbeg = local_tile * tile_vecs;
+      fold_pass<T, Acc, CB, VB, U, false>(p, s, jbeg + threadIdx.x, min(nvec, jbeg + tile_vecs));
+      if (local_tile == 0) {
+        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+        if ((int64_t)threadIdx.x < nhead + ntail) {
+          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
+                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
+          fold_scalar<T, Acc, false>(p, s, i);
+        }
+      }
+    }
+  }
+  if (p.n_ranks > 1) {
+    depart(p, epoch);
+  } else if (p.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) trace_max(p, 2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// push protocol (one position per rank, rank == position): NVLink carries
+// stores only.  Scatter: this rank copies its chunk-q slice of every ring into
+// owner q's staging slot and raises one release flag per 256 KB unit.  Fold:
+// for its own chunk, once every writer's flag for a unit is up, the owner
+// folds its own values and the staged ones in ring order and pushes the mean
+// into all members.  No arrive barrier is needed: a member's chunk reaches
+// the owner only after its kernel started (inputs final), and the owner
+// writes a member's buffer only after receiving that member's data for the
+// same unit.  The depart barrier still closes the cycle.
+
+template <typename T>
+__device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
+  int a = 0, b = nseg - 1;
+  while (a < b) {
+    const int mid = (a + b + 1) >> 1;
+    if (segs[mid].unit0 <= u) a = mid; else b = mid - 1;
+  }
+  return segs[a];
+}
+
+template <typename T, typename Acc, int CB, int VB, int U>
+__global__ void __launch_bounds__(kThreads, 2)
+ring_push_kernel(const __grid_constant__ CycleParams p) {
+  constexpr int N = VB / sizeof(T);
+  constexpr int KC = (U * CB) < 8 ? (U * CB) : 8;  // vectors in flight per thread when copying
+  using Raw = typename RawVec<VB>::type;
+  __shared__ int s_ok;
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) {
+    trace_min(p, 0);
+    trace_max(p, 1);
+    s_epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
+    s_ok = (*(volatile unsigned *)p.status == 0);
+  }
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const int C = p.C, me = p.me;
+  const int64_t n_scatter = (int64_t)(C - 1) * p.scatter_umax;
+  const int64_t n_work = n_scatter + p.ounits[me];
+  const unsigned long long t0 = globaltimer();
+
+  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+    if (!s_ok) break;
+    if (w < n_scatter) {
+      const int r = (int)(w % (C - 1));
+      const int64_t u = w / (C - 1);
+      int q = me + 1 + r;
+      if (q >= C) q -= C;
+      if (u >= p.ounits[q]) continue;
+      const Seg s = find_unit<T>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
+      const int64_t uu = u - s.unit0;
+      const int64_t nvec = (s.body_hi - s.body_lo) / N;
+      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
+      const T *src = static_cast<const T *>(p.src[me]);
+      T *stg = static_cast<T *>(p.stage[q]) + ((int64_t)me * p.stride + s.stage_off - s.lo);
+      for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * KC) {
+        Raw v[KC];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const int64_t j = j0 + (int64_t)c * kThreads;
+          if (j < jend) v[c] = __ldcs(reinterpret_cast<const Raw *>(src + s.body_lo + j * N));
+        }
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const int64_t j = j0 + (int64_t)c * kThreads;
+          if (j < jend) __stcs(reinterpret_cast<Raw *>(stg + s.body_lo + j * N), v[c]);
+        }
+      }
+      if (uu == 0) {
+        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+        if ((int64_t)threadIdx.x < nhead + ntail) {
+          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
+                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
+          stg[i] = src[i];
+        }
+      }
+      __threadfence_system();  // this thread's stores, before the unit flag
+      __syncthreads();
+      if (threadIdx.x == 0)
+        st_release_sys(p.pflags[q] + pflag_index(p.lane, C, me, p.units_max, u), epoch);
+    } else {
+      const int64_t u = w - n_scatter;
+      const Seg s = find_unit<T>(p.segs + p.oseg_base[me], p.oseg_base[me + 1] - p.oseg_base[me], u);
+      if (threadIdx.x == 0) {
+        for (int m = 0; m < C && s_ok; ++m) {
+          if (m == me) continue;
+          const unsigned diag = (2u << 16) | ((unsigned)p.lane << 8) | (unsigned)m;
+          if (!wait_flag(p, p.pflags[me] + pflag_index(p.lane, C, m, p.units_max, u), epoch, t0, diag)) s_ok = 0;
+        }
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      const int64_t uu = u - s.unit0;
+      const int64_t nvec = (s.body_hi - s.body_lo) / N;
+      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
+      for (int64_t j0 = jbeg + threadIdx.x; j0 < jend; j0 += (int64_t)kThreads * U)
+        fold_pass<T, Acc, CB, VB, U, true>(p, s, j0, jend);
+      if (uu == 0) {
+        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+        if ((int64_t)threadIdx.x < nhead + ntail) {
+          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
+                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
+          fold_scalar<T, Acc, true>(p, s, i);
+        }
+      }
+      __syncthreads();  // s_ok is re-armed by thread 0 for the next unit
+    }
+  }
+  depart(p, epoch);
+}
+
+// ---------------------------------------------------------------------------
+// co-resident TMA path (all C members on this device, 16-byte congruent
+// buffers): HBM-bound, so tiles stream through shared memory with bulk async
+// copies.  Warp 0 / lane 0 produces: for each tile it loads the tile of all C
+// members (cp.async.bulk global->shared, completion on a per-stage mbarrier)
+// into a STAGES-deep ring.  Warps 1..8 consume: fold from shared memory in
+// ring order, write the mean tile to shared memory, and one consumer issues
+// C bulk stores (shared->global) of it, double-buffered.  No register
+// staging of loads, so each SM keeps STAGES * C * TV * 16 bytes in flight.
+
+constexpr int kTmaConsumers = 256;
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *smem, const void *gmem, unsigned bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <typename T, typename Acc, int CB, int TV, int STAGES>
+__global__ void __launch_bounds__(kTmaConsumers + 32, 2)
+ring_tma_kernel(const __grid_constant__ CycleParams p) {
+  constexpr int N = 16 / sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][CB][TV]
+  uint4 *out = in + (size_t)STAGES * CB * TV;                          // [2][TV]
+  __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x;
+  const int C = p.C;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    trace_min(p, 0);
+    trace_max(p, 1);
+  }
+  __syncthreads();
+
+  // the tiles this block owns: t = blockIdx.x + i * gridDim.x
+  auto seg_of = [&](int64_t t, int64_t *local) -> Seg {
+    int a = 0, b = p.nseg - 1;
+    while (a < b) {
+      const int mid = (a + b + 1) >> 1;
+      if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
+    }
+    *local = t - __ldg(p.tile_prefix + a);
+    return p.segs[a];
+  };
+
+  if (tid < 32) {
+    if (tid == 0) {  // producer
+      int stage = 0;
+      unsigned phase = 0;
+      int64_t n = 0;
+      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++n) {
+        int64_t lt;
+        const Seg s = seg_of(t, &lt);
+        const int64_t nvec = (s.body_hi - s.body_lo) / N;
+        const int64_t j0 = lt * TV;
+        const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
+        if (n >= STAGES) mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], (unsigned)(cnt * 16 * C));
+        if (cnt > 0) {
+          for (int q = 0; q < C; ++q) {
+            int m = s.k + q;
+            if (m >= C) m -= C;
+            bulk_load(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
+                      (unsigned)(cnt * 16), &full[stage]);
+          }
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // consumers (256 threads)
+  const int c = tid - 32;
+  int stage = 0;
+  unsigned phase = 0;
+  int ob = 0;
+  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+    int64_t lt;
+    const Seg s = seg_of(t, &lt);
+    const int64_t nvec = (s.body_hi - s.body_lo) / N;
+    const int64_t j0 = lt * TV;
+    const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
+    mbar_wait(&full[stage], phase);
+    // consumer 0 finished the previous tile's store bookkeeping (out[ob] free)
+    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+    for (int v = c; v < cnt; v += kTmaConsumers) {
+      Lanes<T, 16> x, o;
+      Acc acc[N];
+      x.raw = in[((size_t)stage * CB + 0) * TV + v];
+#pragma unroll
+      for (int e = 0; e < N; ++e) acc[e] = (Acc)x.v[e];
+#pragma unroll
+      for (int q = 1; q < CB; ++q) {
+        if (q < C) {
+          x.raw = in[((size_t)stage * CB + q) * TV + v];
+#pragma unroll
+          for (int e = 0; e < N; ++e) acc[e] = acc[e] + (Acc)x.v[e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < N; ++e) o.v[e] = finish<T, Acc>(acc[e], p);
+      out[ob * TV + v] = o.raw;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+    if (c == 0) {
+      mbar_arrive(&empty[stage]);  // every consumer has read this stage
+      if (cnt > 0) {
+        for (int q = 0; q < C; ++q)
+          bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // out[ob ^ 1] reusable
+    }
+    if (lt == 0) {
+      const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+      if ((int64_t)c < nhead + ntail) {
+        const int64_t i = (int64_t)c < nhead ? s.lo + c : s.body_hi + ((int64_t)c - nhead);
+        fold_scalar<T, Acc, false>(p, s, i);
+      }
+    }
+    ob ^= 1;
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  if (c == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    trace_max(p, 2);
+  }
+}
+
+// live <- mean + (live - snap); exactly mean where live == snap bitwise.
+template <typename T, typename U>
+__global__ void __launch_bounds__(kThreads)
+blend_kernel(T *__restrict__ live, const T *__restrict__ snap, const T *__restrict__ mean, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T l = live[i], s = snap[i], m = __ldcs(mean + i);
+    U lb, sb;
+    memcpy(&lb, &l, sizeof(T));
+    memcpy(&sb, &s, sizeof(T));
+    live[i] = (lb == sb) ? m : (m + (l - s));
+  }
+}
+
+template <typename T, typename U>
+__global__ void __launch_bounds__(kThreads)
+blend_kernel_v4(T *__restrict__ live, const T *__restrict__ snap, const T *__restrict__ mean, int64_t nvec) {
+  constexpr int N = 16 / sizeof(T);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nvec; j += stride) {
+    Lanes<T, 16> l, s, m, o;
+    l.raw = *reinterpret_cast<const uint4 *>(live + j * N);
+    s.raw = __ldcs(reinterpret_cast<const uint4 *>(snap + j * N));
+    m.raw = __ldcs(reinterpret_cast<const uint4 *>(mean + j * N));
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      U lb, sb;
+      memcpy(&lb, &l.v[e], sizeof(T));
+      memcpy(&sb, &s.v[e], sizeof(T));
+      o.v[e] = (lb == sb) ? m.v[e] : (m.v[e] + (l.v[e] - s.v[e]));
+    }
+    *reinterpret_cast<uint4 *>(live + j * N) = o.raw;
+  }
+}
