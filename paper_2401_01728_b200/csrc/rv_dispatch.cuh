@@ -68,7 +68,7 @@ KernelFn pick_tma(int c, int *tv_out) {
 
 KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
   // RAVNEST_B200_TMA_VARIANT (experiments): 1 = 6 stages, 2 = 4 stages (one
-  // block per SM), 3 = 8 stages of 16 KB
+  // block per SM), 3 = 8 stages of 16 KB, 4 = L2 evict-first hints
   const char *ve = getenv("RAVNEST_B200_TMA_VARIANT");
   const int v = ve ? atoi(ve) : 0;
   int stages = kTmaStages;
@@ -76,6 +76,11 @@ KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
   if (v > 0 && mode == kF32Acc64) {
     if (v == 1) { stages = 6; k = pick_tma<float, double, 6, kTmaStageBytes>(c, tv_out); }
     else if (v == 2) { stages = 4; k = pick_tma<float, double, 4, kTmaStageBytes>(c, tv_out); }
+    else if (v == 4) {
+      k = c <= 8 ? (KernelFn)ring_tma_kernel<float, double, 8, kTmaStageBytes / (8 * 16), kTmaStages, true>
+                 : pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out);
+      *tv_out = c <= 8 ? kTmaStageBytes / (8 * 16) : *tv_out;
+    }
     else { stages = 8; k = pick_tma<float, double, 8, 16 * 1024>(c, tv_out); }
   } else {
     k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out)

@@ -226,13 +226,35 @@ __device__ __forceinline__ void bulk_load(void *smem, const void *gmem, unsigned
                : "memory");
 }
 
+__device__ __forceinline__ void bulk_load_hint(void *smem, const void *gmem, unsigned bytes, unsigned long long *bar,
+                                               unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store_hint(void *gmem, const void *smem, unsigned bytes,
+                                                unsigned long long policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem),
+               "r"(smem_addr(smem)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)),
                "r"(bytes)
                : "memory");
 }
 
-template <typename T, typename Acc, int CB, int TV, int STAGES>
+template <typename T, typename Acc, int CB, int TV, int STAGES, bool HINT = false>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 2)
 ring_tma_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = 16 / sizeof(T);
@@ -281,8 +303,12 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
           for (int q = 0; q < C; ++q) {
             int m = s.k + q;
             if (m >= C) m -= C;
-            bulk_load(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
-                      (unsigned)(cnt * 16), &full[stage]);
+            if constexpr (HINT)
+              bulk_load_hint(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
+                             (unsigned)(cnt * 16), &full[stage], evict_first_policy());
+            else
+              bulk_load(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
+                        (unsigned)(cnt * 16), &full[stage]);
           }
         }
         if (++stage == STAGES) {
@@ -332,7 +358,11 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
       mbar_arrive(&empty[stage]);  // every consumer has read this stage
       if (cnt > 0) {
         for (int q = 0; q < C; ++q)
-          bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16));
+          if constexpr (HINT)
+            bulk_store_hint(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16),
+                            evict_first_policy());
+          else
+            bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16));
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // out[ob ^ 1] reusable
