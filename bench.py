@@ -528,6 +528,22 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te[0])
 
+    phases = None
+    if args.trace:
+        # device-side phase split of a few isolated cycles (max over ranks)
+        grp.plan.set_trace(True)
+        acc = torch.zeros(4, dtype=torch.float64)
+        for _ in range(5):
+            dist.barrier()
+            step()
+            torch.cuda.synchronize()
+            tr = grp.plan.read_trace(0)
+            acc += torch.tensor([tr["ready_us"], tr["data_us"], tr["depart_us"], tr["total_us"]], dtype=torch.float64)
+        grp.plan.set_trace(False)
+        acc /= 5
+        dist.all_reduce(acc, op=dist.ReduceOp.MAX)
+        phases = {k: round(float(v), 2) for k, v in zip(("ready", "data", "depart", "total"), acc)}
+
     nccl = None
     if args.nccl:
         nccl = nccl_compare(lens, x, world, min(args.steps, 20))
@@ -565,6 +581,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
         }
         if nccl:
             line["nccl_compare"] = nccl
+        if phases:
+            line["phases_us"] = phases
         print(json.dumps(line), flush=True)
     grp_e2e.close()
     grp.close()
@@ -620,6 +638,7 @@ def main():
     ap.add_argument("--nccl", type=int, default=1)
     ap.add_argument("--blend", type=int, default=0, help="config 4: snapshot average + delayed-update blend")
     ap.add_argument("--tau", type=int, default=4)
+    ap.add_argument("--trace", type=int, default=1, help="N>1: add a device-side phase trace")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
