@@ -178,3 +178,31 @@ def floor1_rel_err(got: np.ndarray, want: np.ndarray) -> float:
     if got.size == 0:
         return 0.0
     return float((np.abs(got - want) / np.maximum(np.abs(want), 1.0)).max())
+
+
+def random_instance(rng: np.random.Generator, n_clusters: int, max_peers: int = 4, max_dim: int = 4096):
+    """Restates multiring.random_instance (multiring.py:440-465): random nested
+    per-cluster layouts and N(0, 10) cluster vectors, drawing from ``rng`` in
+    the same order, so a Philox key reproduces the reference's instance
+    stream (pinned against tests/golden crit1_* fixtures).  Returns
+    (layouts {cid: [(start, len), ...]}, values {cid: float64[dim]})."""
+    p_max = int(rng.integers(1, max_peers + 1))
+    lo = max(p_max, 2)
+    dim = max(int(np.exp(rng.uniform(np.log(lo), np.log(max_dim)))), p_max)
+    master = sorted(rng.choice(np.arange(1, dim), size=p_max - 1, replace=False).tolist()) if p_max > 1 else []
+    layouts = {}
+    for cid in range(n_clusters):
+        cuts = list(master) if cid == 0 else [c for c in master if rng.random() < 0.5]
+        edges = [0, *cuts, dim]
+        layouts[cid] = [(edges[i], edges[i + 1] - edges[i]) for i in range(len(edges) - 1)]
+    values = {cid: rng.normal(0.0, 10.0, size=dim) for cid in range(n_clusters)}
+    return layouts, values
+
+
+def rings_of_layouts(layouts) -> tuple[list[int], list[int]]:
+    """Ring (start, length) lists for nested layouts: the union of all
+    clusters' cuts (multiring.py:80-105)."""
+    cuts = sorted({s for lay in layouts.values() for s, _ in lay if s > 0})
+    total = sum(n for _, n in next(iter(layouts.values())))
+    edges = [0, *cuts, total]
+    return edges[:-1], [edges[i + 1] - edges[i] for i in range(len(edges) - 1)]

@@ -331,3 +331,43 @@ def test_local_group_several_clusters_per_device():
         rv.ring_mean_(sched, ts)
         got = np.stack([ts[m].cpu().numpy() for m in range(c)])
         assert bits_equal(got, want), placement
+
+
+def test_acceptance_criterion_1_on_gpu():
+    # test_acceptance.py:28-51 run through the drop-in on the GPU: the same
+    # 1000 Philox-777 instances (C in 2..6, dims <= 4096, N(0,10)); every
+    # result bitwise equal to the pinned oracle and within 1e-12 of the
+    # scalar mean on the reference's floor-1 metric, 2(C-1) rounds
+    rng = np.random.Generator(np.random.Philox(key=777))
+    worst = 0.0
+    for _ in range(1000):
+        c = int(rng.integers(2, 7))
+        layouts, values = ring_oracle.random_instance(rng, c, max_peers=4, max_dim=4096)
+        sched = rv.build_ring_schedule({cid: [rv.ParamRange(s, n) for s, n in lay] for cid, lay in layouts.items()})
+        out, stats = rv.run_allreduce(sched, values)
+        starts, lens = ring_oracle.rings_of_layouts(layouts)
+        want = ring_oracle.ring_mean(starts, lens, [values[k] for k in range(c)])
+        mean = np.mean([values[k] for k in range(c)], axis=0)
+        for k in range(c):
+            assert bits_equal(out[k], want[k])
+            worst = max(worst, ring_oracle.floor1_rel_err(out[k], mean))
+        assert all(s.rounds == 2 * (c - 1) for s in stats)
+    assert worst <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_wide_instances_all_modes(seed):
+    # C up to 16, ragged nested layouts, fp32 (both folds) and fp64, in place
+    rng = np.random.Generator(np.random.Philox(key=9000 + seed))
+    for _ in range(25):
+        c = int(rng.integers(2, 17))
+        layouts, values = ring_oracle.random_instance(rng, c, max_peers=6, max_dim=20000)
+        starts, lens = ring_oracle.rings_of_layouts(layouts)
+        sched = make_sched(lens, c)
+        rows64 = [values[k] for k in range(c)]
+        rows32 = [v.astype(np.float32) for v in rows64]
+        assert bits_equal(run_inplace(sched, rows64, torch.float64), np.stack(ring_oracle.ring_mean(starts, lens, rows64)))
+        want = np.stack(ring_oracle.ring_mean(starts, lens, rows32)).astype(np.float32)
+        assert bits_equal(run_inplace(sched, rows32, torch.float32), want)
+        want = np.stack(ring_oracle.ring_mean(starts, lens, rows32, acc="native"))
+        assert bits_equal(run_inplace(sched, rows32, torch.float32, acc="native"), want)
