@@ -367,7 +367,6 @@ def run_single(args):
     # e2e: host (pinned) buffers -> device -> average -> host, via the C ABI
     hsrc = [x.cpu().pin_memory() for x in xs]
     hdst = [torch.empty_like(h).pin_memory() for h in hsrc]
-    plan = g.plans[0]
     e2e_streams = [torch.cuda.Stream() for _ in range(len(lens))]
     plan_e2e = LocalRingGroup(ring_starts(lens), lens, total, [0] * c, torch.float32, acc=args.acc,
                               lanes=len(lens))
@@ -396,7 +395,6 @@ def run_single(args):
     torch.cuda.synchronize()
     plan_e2e.check()
     e2e_ms = a.elapsed_time(b) / e_steps
-    del plan
 
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -530,23 +528,10 @@ def run_multi(args, rank: int, world: int, local_rank: int):
 
     phases = None
     if args.trace:
-        # device-side phase split of a few isolated cycles (max over ranks)
-        grp.plan.set_trace(True)
-        acc = torch.zeros(4, dtype=torch.float64)
-        for _ in range(5):
-            dist.barrier()
-            step()
-            torch.cuda.synchronize()
-            tr = grp.plan.read_trace(0)
-            acc += torch.tensor([tr["ready_us"], tr["data_us"], tr["depart_us"], tr["total_us"]], dtype=torch.float64)
-        grp.plan.set_trace(False)
-        acc /= 5
-        dist.all_reduce(acc, op=dist.ReduceOp.MAX)
-        phases = {k: round(float(v), 2) for k, v in zip(("ready", "data", "depart", "total"), acc)}
-
+        phases = optional_leg("trace", lambda: trace_phases(grp, step))
     nccl = None
     if args.nccl:
-        nccl = nccl_compare(lens, x, world, min(args.steps, 20))
+        nccl = optional_leg("nccl_compare", lambda: nccl_compare(lens, x, world, min(args.steps, 20)))
 
     if rank == 0:
         c = world
@@ -586,6 +571,35 @@ def run_multi(args, rank: int, world: int, local_rank: int):
         print(json.dumps(line), flush=True)
     grp_e2e.close()
     grp.close()
+
+
+def optional_leg(name: str, fn):
+    """Informational legs (NCCL comparison, phase trace) must never suppress
+    the headline line: report a failure in the JSON instead of raising."""
+    try:
+        return fn()
+    except Exception as e:  # pragma: no cover - diagnostic path
+        print(f"[bench] optional leg {name} failed: {e!r}", file=sys.stderr, flush=True)
+        return {"error": repr(e)[:200]}
+
+
+def trace_phases(grp, step):
+    """Device-side phase split of a few isolated cycles, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    grp.plan.set_trace(True)
+    acc = torch.zeros(4, dtype=torch.float64)
+    for _ in range(5):
+        dist.barrier()
+        step()
+        torch.cuda.synchronize()
+        tr = grp.plan.read_trace(0)
+        acc += torch.tensor([tr["ready_us"], tr["data_us"], tr["depart_us"], tr["total_us"]], dtype=torch.float64)
+    grp.plan.set_trace(False)
+    acc /= 5
+    dist.all_reduce(acc, op=dist.ReduceOp.MAX)
+    return {k: round(float(v), 2) for k, v in zip(("ready", "data", "depart", "total"), acc)}
 
 
 def nccl_compare(lens, x, world: int, steps: int):
