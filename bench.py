@@ -603,36 +603,12 @@ def trace_phases(grp, step):
 
 
 def nccl_compare(lens, x, world: int, steps: int):
-    """NCCL comparison path: ncclAllReduce(avg) per ring on its own buffer
-    slice (one communicator; rings issued back to back).  Not parity-exact."""
-    import torch
-    import torch.distributed as dist
+    """NCCL comparison (tools/nccl_compare.py): ncclAllReduce(avg) per ring,
+    sequential on one communicator and concurrent with a communicator and a
+    stream per ring; the faster one is the headline comparison."""
+    from tools.nccl_compare import NcclRings
 
-    y = x.clone()
-    starts = ring_starts(lens)
-    views = [y[s:s + n] for s, n in zip(starts, lens)]
-
-    def step():
-        for v in views:
-            dist.all_reduce(v, op=dist.ReduceOp.AVG)
-
-    for _ in range(3):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    s = torch.cuda.current_stream()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record(s)
-    for _ in range(steps):
-        step()
-    b.record(s)
-    torch.cuda.synchronize()
-    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t[0])
-    return {"ms_per_step": round(ms, 4), "bus_gbps_per_gpu": round(busbw(sum(lens), world, ms * 1e-3), 3),
-            "algo": os.environ.get("NCCL_ALGO", "default")}
+    return NcclRings(x, lens).report(steps)
 
 
 def main():

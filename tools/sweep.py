@@ -20,6 +20,7 @@ import torch.distributed as dist
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2401_01728_b200.dist import DistRingGroup  # noqa: E402
+from tools.nccl_compare import NcclRings  # noqa: E402
 
 
 def busbw(total, c, sec):
@@ -101,16 +102,10 @@ def main():
                                                 zip(("ready", "data", "depart", "total"), acc)}}
                     del graph
                     g.close()
-                views = [x[s:s + n] for s in starts]
-
-                def nccl():
-                    for v in views:
-                        dist.all_reduce(v, op=dist.ReduceOp.AVG)
-
-                for _ in range(3):
-                    nccl()
-                ms = timed(nccl, args.steps, stream)
-                row["nccl"] = {"ms": round(ms, 5), "bus_gbps": round(busbw(total, world, ms * 1e-3), 2)}
+                rep = NcclRings(x, lens).report(args.steps)
+                row["nccl"] = {"ms": rep["ms_per_step"], "bus_gbps": rep["bus_gbps_per_gpu"], "best": rep["best"],
+                               "sequential_ms": rep["sequential"]["ms_per_step"],
+                               "concurrent_ms": rep["concurrent"]["ms_per_step"]}
             if rank == 0:
                 print(json.dumps(row), flush=True)
                 lines.append(row)
