@@ -604,8 +604,8 @@ def trace_phases(grp, step):
 
 def nccl_compare(lens, x, world: int, steps: int):
     """NCCL comparison (tools/nccl_compare.py): ncclAllReduce(avg) per ring,
-    sequential on one communicator and concurrent with a communicator and a
-    stream per ring; the faster one is the headline comparison."""
+    issued back to back and coalesced into one NCCL group; the faster one is
+    the headline comparison."""
     from tools.nccl_compare import NcclRings
 
     return NcclRings(x, lens).report(steps)

@@ -6,8 +6,14 @@ parameter vector:
 
 * ``sequential`` -- one communicator, the rings issued back to back on one
   stream (what a straightforward port would do);
-* ``concurrent`` -- one communicator per ring, every ring on
-  its own stream, all in flight together.
+* ``coalesced`` -- all rings' all-reduces in one NCCL group
+  (ncclGroupStart/End via torch's coalescing manager), so they run
+  concurrently on one communicator.
+
+A communicator and stream per ring was measured too
+(profiles/r01/sweep_n4_nccl_multicomm.jsonl: 645-668 GB/s at >= 256 MiB at 4
+GPUs), but concurrent collectives on separate communicators can deadlock --
+it did, at 256 MiB x 2 rings -- so it is not part of the default paths.
 
 Timed with CUDA events, max over ranks.
 """
@@ -15,17 +21,6 @@ Timed with CUDA events, max over ranks.
 from __future__ import annotations
 
 import os
-
-
-_GROUPS: list = []  # one NCCL communicator per ring index, created once per process
-
-
-def _ring_groups(n: int) -> list:
-    import torch.distributed as dist
-
-    while len(_GROUPS) < n:
-        _GROUPS.append(dist.new_group(backend="nccl"))
-    return _GROUPS[:n]
 
 
 def _busbw(total_params: int, c: int, seconds: float) -> float:
@@ -45,8 +40,7 @@ class NcclRings:
             starts.append(s)
             s += n
         self.views = [self.y[a:a + n] for a, n in zip(starts, self.lens)]
-        self.groups = _ring_groups(len(self.lens))
-        self.streams = [torch.cuda.Stream() for _ in self.lens]
+        self.device = x.device
 
     def sequential(self):
         import torch.distributed as dist
@@ -54,17 +48,12 @@ class NcclRings:
         for v in self.views:
             dist.all_reduce(v, op=dist.ReduceOp.AVG)
 
-    def concurrent(self):
-        import torch
+    def coalesced(self):
         import torch.distributed as dist
 
-        main = torch.cuda.current_stream()
-        for v, g, st in zip(self.views, self.groups, self.streams):
-            st.wait_stream(main)
-            with torch.cuda.stream(st):
-                dist.all_reduce(v, op=dist.ReduceOp.AVG, group=g)
-        for st in self.streams:
-            main.wait_stream(st)
+        with dist._coalescing_manager(device=self.device):
+            for v in self.views:
+                dist.all_reduce(v, op=dist.ReduceOp.AVG)
 
     def time(self, fn, steps: int) -> float:
         import torch
@@ -89,12 +78,12 @@ class NcclRings:
     def report(self, steps: int) -> dict:
         out = {"algo": os.environ.get("NCCL_ALGO", "default"),
                "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default")}
-        for name, fn in (("sequential", self.sequential), ("concurrent", self.concurrent)):
+        for name, fn in (("sequential", self.sequential), ("coalesced", self.coalesced)):
             ms = self.time(fn, steps)
             out[name] = {"ms_per_step": round(ms, 4),
                          "bus_gbps_per_gpu": round(_busbw(sum(self.lens), self.world, ms * 1e-3), 3)}
         # headline comparison: the faster NCCL variant
-        best = min(("sequential", "concurrent"), key=lambda k: out[k]["ms_per_step"])
+        best = min(("sequential", "coalesced"), key=lambda k: out[k]["ms_per_step"])
         out["ms_per_step"] = out[best]["ms_per_step"]
         out["bus_gbps_per_gpu"] = out[best]["bus_gbps_per_gpu"]
         out["best"] = best

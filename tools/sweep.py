@@ -105,7 +105,7 @@ def main():
                 rep = NcclRings(x, lens).report(args.steps)
                 row["nccl"] = {"ms": rep["ms_per_step"], "bus_gbps": rep["bus_gbps_per_gpu"], "best": rep["best"],
                                "sequential_ms": rep["sequential"]["ms_per_step"],
-                               "concurrent_ms": rep["concurrent"]["ms_per_step"]}
+                               "coalesced_ms": rep["coalesced"]["ms_per_step"]}
             if rank == 0:
                 print(json.dumps(row), flush=True)
                 lines.append(row)
