@@ -21,6 +21,46 @@ def bits(a):
     return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
 
 
+def stall_phase(rank, world, local):
+    """Failure detection: only rank 0 launches a cycle; its kernel must give
+    up after the timeout with a StallError naming a missing peer (no GPU
+    hang).  Afterwards a fresh group must work normally."""
+    from paper_2401_01728_b200.errors import StallError
+
+    failures = 0
+    lens = [4097, 333]
+    total = sum(lens)
+    for proto in ("pull", "push"):
+        x = torch.full((total,), float(rank), device=f"cuda:{local}")
+        g = DistRingGroup(src=x, starts=[0, lens[0]], lens=lens, protocol=proto, timeout_s=0.5)
+        if rank == 0:
+            g.average()
+            torch.cuda.synchronize()
+            try:
+                g.check()
+                print(f"rank 0 {proto}: expected a StallError", flush=True)
+                failures += 1
+            except StallError as e:
+                if "rank" not in str(e):
+                    print(f"rank 0 {proto}: stall message lacks the rank: {e}", flush=True)
+                    failures += 1
+        dist.barrier()
+        g.close()
+        # a fresh group works
+        x.fill_(float(rank))
+        g = DistRingGroup(src=x, starts=[0, lens[0]], lens=lens, protocol=proto)
+        g.average()
+        torch.cuda.synchronize()
+        g.check()
+        want = np.float32(sum(range(world)) / world)
+        if not (x.cpu().numpy() == want).all():
+            print(f"rank {rank} {proto}: fresh group after a stall is wrong", flush=True)
+            failures += 1
+        dist.barrier()
+        g.close()
+    return failures
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -116,6 +156,7 @@ def main():
                     failures += 1
             dist.barrier()
             g.close()
+    failures += stall_phase(rank, world, local)
     t = torch.tensor([failures])
     dist.all_reduce(t)
     if rank == 0:
