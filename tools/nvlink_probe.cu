@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <string>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -305,6 +306,18 @@ int main(int argc, char **argv) {
     CK(cudaMalloc(&scratch[g], (size_t)chunk_vecs * 16));
   }
   printf("GPUs %d, %lld bytes per member, chunk %lld bytes\n", ng, total_bytes, chunk_vecs * 16);
+  if (argc > 2) {
+    // single pattern, few launches (for ncu: nvlrx/nvltx user vs protocol bytes)
+    const std::string m = argv[2];
+    double r = 0;
+    if (m == "write") r = run<4, 1>(ng, bufs, scratch, chunk_vecs, 2, 2);
+    else if (m == "read") r = run<4, 0>(ng, bufs, scratch, chunk_vecs, 2, 2);
+    else if (m == "mixed") r = run<4, 2>(ng, bufs, scratch, chunk_vecs, 2, 2);
+    else if (m == "bulkstore") r = run_bulk<3>(ng, bufs, chunk_vecs * 16, 2, 2);
+    else if (m == "bulkload") r = run_bulk<4>(ng, bufs, chunk_vecs * 16, 2, 2);
+    printf("%s %.1f GB/s per GPU per direction\n", m.c_str(), r);
+    return 0;
+  }
   const int iters = 20;
   for (int bps : {1, 2, 4}) {
     printf("blocks/SM %d: read U4 %.1f  U8 %.1f | write U4 %.1f U8 %.1f | mixed U2 %.1f U4 %.1f GB/s per GPU per direction\n",
