@@ -161,7 +161,7 @@ class LocalRingGroup:
     """
 
     def __init__(self, starts: Sequence[int], lens: Sequence[int], total: int, devices: Sequence[int],
-                 dtype, acc: str = "f64", lanes: int = 1):
+                 dtype, acc: str = "f64", lanes: int = 1, protocol: str = "pull"):
         self.starts = [int(s) for s in starts]
         self.lens = [int(n) for n in lens]
         self.total = int(total)
@@ -189,6 +189,19 @@ class LocalRingGroup:
             areas = [self.plans[d].flag_area()[0] for d in self.device_order]
             for rank, d in enumerate(self.device_order):
                 self.plans[d].set_peers(rank, len(self.device_order), areas)
+        self.protocol = protocol if len(self.device_order) > 1 else "pull"
+        if self.protocol == "push":
+            # store-only transport: one cluster per device, position == rank
+            if sorted(self.devices) != self.devices or len(set(self.devices)) != len(self.devices):
+                raise ConfigError("push needs one cluster per device, in device order")
+            push = []
+            for d in self.device_order:
+                self.plans[d].set_protocol("push")
+                push.append(self.plans[d].push_area()[0])
+            for d in self.device_order:
+                self.plans[d].set_push_peers(push)
+        elif self.protocol != "pull":
+            raise ConfigError(f"unknown protocol {protocol!r}")
 
     def bind(self, pos: int, src_ptr: int, dst_ptr: int) -> None:
         for plan in self.plans.values():

@@ -12,9 +12,10 @@ from bench import WORKLOADS, ring_starts, synth  # noqa: E402
 from paper_2401_01728_b200.plan import LocalRingGroup  # noqa: E402
 
 lens = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "bert"]
+proto = sys.argv[2] if len(sys.argv) > 2 else "pull"
 total = sum(lens)
 xs = [synth(total, m, torch.device(f"cuda:{m}")) for m in range(2)]
-g = LocalRingGroup(ring_starts(lens), lens, total, [0, 1], torch.float32)
+g = LocalRingGroup(ring_starts(lens), lens, total, [0, 1], torch.float32, protocol=proto)
 g.bind_tensors(xs)
 streams = {d: torch.cuda.Stream(device=d) for d in (0, 1)}
 for _ in range(5):
@@ -33,4 +34,4 @@ with torch.cuda.device(1):
 for d in (0, 1):
     torch.cuda.synchronize(d)
 ms = ev[0].elapsed_time(ev[1]) / 10
-print(f"profile_p2p: {ms:.4f} ms per cycle, {total * 4 / ms / 1e6:.1f} GB/s busbw (C=2)")
+print(f"profile_p2p {proto}: {ms:.4f} ms per cycle, {total * 4 / ms / 1e6:.1f} GB/s busbw (C=2)")
