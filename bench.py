@@ -45,6 +45,9 @@ WORKLOAD_NAMES = {
 }
 METRIC = "param-averaging bus GB/s and ms/round at 1/2/4/8 B200 vs NVLink roofline"
 NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
+# user-data ceilings of each transport's traffic pattern: ~840 GB/s raw per
+# direction / (1 + protocol overhead), ncu-measured (profiles/r01/ncu_nvlink.md)
+PATTERN_CEILING_GBS = {"push": 706.0, "pull": 656.0}
 SEED = 20241018
 SIGMA = 0.02
 
@@ -554,7 +557,10 @@ def run_multi(args, rank: int, world: int, local_rank: int):
                        "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
                        "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
-                         "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
+                         "traffic": ncu_traffic(args.workload, c, world, args.acc) if grp.protocol == "push" else None,
+                         "pattern_ceiling": PATTERN_CEILING_GBS[grp.protocol],
+                         "frac_of_pattern_ceiling": round(achieved / PATTERN_CEILING_GBS[grp.protocol], 4),
                          "basis": f"2(C-1)/C*S = {int(alg_bytes)} B per GPU per launch, each direction",
                          "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)"},
             "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3) * world, 3), "unit": "GB/s",
