@@ -193,6 +193,10 @@ int upload(rv_plan::Lane &lane, const std::vector<Seg> &segs, const std::vector<
   return RV_OK;
 }
 
+// push: target work items (scatter + fold units) per resident block; more
+// items shrink the tail when blocks finish unevenly, fewer amortise flags
+constexpr int64_t kPushItemsPerBlock = 2;
+
 int build_tables(rv_plan *p) {
   for (int i = 0; i < p->C; ++i)
     if (!p->bound[i]) return set_err(RV_E_ARG, "cluster position %d is not bound", i);
@@ -257,7 +261,9 @@ int build_tables(rv_plan *p) {
       }
       owner_elems = std::max(owner_elems, e);
     }
-    const int64_t items = std::max<int64_t>(1, 2LL * p->sm_count * p->occ);
+    const char *ie = getenv("RAVNEST_B200_PUSH_ITEMS");  // work items per resident block (tuning)
+    const int64_t per_block = ie ? std::max(1, atoi(ie)) : kPushItemsPerBlock;
+    const int64_t items = std::max<int64_t>(1, per_block * p->sm_count * p->occ);
     const int64_t want = (owner_elems / N * (p->C - 1) + items - 1) / items;
     const int64_t lo = kMinUnitBytes / (N * es), hi = kUnitBytes / (N * es);
     unit_vecs = std::min(hi, std::max(lo, (want + kThreads - 1) / kThreads * kThreads));
