@@ -108,6 +108,8 @@ class DistRingGroup:
                 raise LayoutError(f"buffer has {t.numel()} elements, schedule expects {total}")
         if dst.dtype != src.dtype:
             raise LayoutError("src and dst dtypes differ")
+        if total == 0:
+            raise LayoutError("DistRingGroup needs a non-empty parameter vector")
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)

@@ -93,6 +93,8 @@ def ring_mean_(schedule, tensors: dict, acc: str = "f64", lanes: int = 1, stream
             raise LayoutError("ring_mean_ needs CUDA tensors; use apply_ring_mean for host arrays")
         if t.dtype != dtype:
             raise LayoutError(f"mixed dtypes {t.dtype} and {dtype}")
+    if schedule.total_params == 0:
+        return tensors  # nothing to average (all rings empty)
     devices = [t.device.index for t in ts]
     g = group_for(schedule, devices, dtype, acc=acc, lanes=lanes)
     g.bind_tensors(ts)

@@ -382,3 +382,21 @@ def test_random_wide_instances_all_modes(seed):
         assert bits_equal(run_inplace(sched, rows32, torch.float32), want)
         want = np.stack(ring_oracle.ring_mean(starts, lens, rows32, acc="native"))
         assert bits_equal(run_inplace(sched, rows32, torch.float32, acc="native"), want)
+
+
+def test_empty_vectors_and_cluster_limits():
+    # rings of length 0 everywhere (total 0): a no-op, like the reference
+    sched = make_sched([0, 0], 3)
+    ts = {m: torch.empty(0, device="cuda") for m in range(3)}
+    assert rv.ring_mean_(sched, ts) is ts
+    out = rv.apply_ring_mean(sched, {m: np.zeros(0) for m in range(3)})
+    assert all(v.shape == (0,) and v.dtype == np.float64 for v in out.values())
+    # the largest supported cluster count, and one more
+    c = _native.RV_MAX_CLUSTERS
+    lens = [1000, 7]
+    rows = [np.full(sum(lens), float(m), dtype=np.float32) for m in range(c)]
+    got = run_inplace(make_sched(lens, c), rows, torch.float32)
+    want = np.stack(ring_oracle.ring_mean([0, lens[0]], lens, rows)).astype(np.float32)
+    assert bits_equal(got, want)
+    with pytest.raises(rv.ConfigError):
+        DevicePlan(0, c + 1, [0], [10], 10, _native.RV_DTYPE_F32)
