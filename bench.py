@@ -370,9 +370,9 @@ def run_single(args):
     # e2e: host (pinned) buffers -> device -> average -> host, via the C ABI
     hsrc = [x.cpu().pin_memory() for x in xs]
     hdst = [torch.empty_like(h).pin_memory() for h in hsrc]
-    e2e_streams = [torch.cuda.Stream() for _ in range(len(lens))]
+    e2e_streams = [torch.cuda.Stream() for _ in range(args.e2e_lanes)]
     plan_e2e = LocalRingGroup(ring_starts(lens), lens, total, [0] * c, torch.float32, acc=args.acc,
-                              lanes=len(lens))
+                              lanes=args.e2e_lanes)
     plan_e2e.bind_tensors(xs)
     pe = plan_e2e.plans[0]
 
@@ -432,7 +432,7 @@ def run_single(args):
         "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3), 3), "unit": "GB/s",
                 "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": c * total * 4, "d2h_bytes_per_step": c * total * 4,
-                "path": "rv_allreduce_mean_host (pinned host fp32, per-ring lanes)"},
+                "path": f"rv_allreduce_mean_host (pinned host fp32, {args.e2e_lanes} pipelined lanes)"},
         "gpu_launches": args.steps * (args.lanes + (c if args.blend else 0)),
         "clocks": clk,
     }
@@ -501,9 +501,9 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     # e2e through the host-buffer C ABI: pinned host -> GPU -> average -> host
     hsrc = x.cpu().pin_memory()
     hdst = torch.empty_like(hsrc).pin_memory()
-    grp_e2e = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=len(lens),
+    grp_e2e = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.e2e_lanes,
                             protocol=args.protocol)
-    e2e_streams = [torch.cuda.Stream() for _ in lens]
+    e2e_streams = [torch.cuda.Stream() for _ in range(args.e2e_lanes)]
 
     def e2e_step():
         for s in e2e_streams:
@@ -566,7 +566,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3) * world, 3), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": world * total * 4, "d2h_bytes_per_step": world * total * 4,
-                    "path": "rv_allreduce_mean_host (pinned host fp32, per-ring lanes)"},
+                    "path": f"rv_allreduce_mean_host (pinned host fp32, {args.e2e_lanes} pipelined lanes)"},
             "gpu_launches": args.steps * (args.lanes + (1 if args.blend else 0)) * world,
             "clocks": clk,
         }
@@ -635,6 +635,7 @@ def main():
     ap.add_argument("--blend", type=int, default=0, help="config 4: snapshot average + delayed-update blend")
     ap.add_argument("--tau", type=int, default=4)
     ap.add_argument("--trace", type=int, default=1, help="N>1: add a device-side phase trace")
+    ap.add_argument("--e2e-lanes", type=int, default=16, help="pipeline stages of the host-buffer path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

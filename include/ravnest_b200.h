@@ -93,8 +93,11 @@ int rv_plan_bind(rv_plan *plan, int pos, const void *src, void *dst);
 /* Positions hosted by this device: their chunks are folded here. */
 int rv_plan_set_local(rv_plan *plan, const int *positions, int n_positions);
 
-/* 1 = one launch covers all rings; n_rings = one launch per ring (ring r on
- * stream r % n_streams), the north-star "one stream per ring". */
+/* A lane is a contiguous element range averaged by one launch on its own
+ * stream (lane l on stream l % n_streams).  1 = one launch for everything;
+ * n_rings = one launch per ring (the north-star "one stream per ring");
+ * fewer lanes group consecutive rings, more lanes (up to max(64, n_rings))
+ * cut rings into equal pieces -- finer host-buffer pipelining. */
 int rv_plan_set_lanes(rv_plan *plan, int n_lanes);
 
 /* This plan's flag area (device memory, cudaMalloc'd: IPC-exportable). */

@@ -110,7 +110,8 @@ struct rv_plan {
     int nseg = 0;
     int64_t n_tiles = 0;
     int64_t elems = 0;
-    std::vector<int> rings;
+    int64_t lo = 0, hi = 0;  // element range of this lane
+    std::vector<int> rings;  // rings meeting the range
     int grid = 0;
     // push
     int64_t stride = 0, unit_vecs = 0, scatter_umax = 0;
@@ -162,22 +163,65 @@ void set_body(Seg &s, int N, int64_t a0) {
 
 bool push_active(const rv_plan *p) { return p->proto == RV_PROTO_PUSH && p->n_ranks > 1; }
 
+// Lane l is the element range [first, second) of the parameter vector that
+// one launch (on its own stream) averages.  n_lanes <= R: consecutive whole
+// rings per lane (n_lanes == R is one ring per lane); n_lanes > R: every ring
+// is cut into equal pieces, more pieces for longer rings.
+std::vector<std::pair<int64_t, int64_t>> lane_ranges(const rv_plan *p) {
+  const int L = p->n_lanes, R = p->R;
+  std::vector<std::pair<int64_t, int64_t>> out;
+  if (R == 0) {
+    out.assign(L, {0, 0});
+    return out;
+  }
+  if (L <= R) {
+    for (int l = 0; l < L; ++l) {
+      const int r0 = (int)((int64_t)l * R / L), r1 = (int)((int64_t)(l + 1) * R / L);
+      out.push_back({p->rstart[r0], p->rstart[r1 - 1] + p->rlen[r1 - 1]});
+    }
+    return out;
+  }
+  std::vector<int> pieces(R, 1);
+  int left = L - R;
+  const int64_t total = std::max<int64_t>(1, p->total);
+  for (int r = 0; r < R && left > 0; ++r) {
+    const int extra = (int)std::min<int64_t>(left, (int64_t)(L - R) * p->rlen[r] / total);
+    pieces[r] += extra;
+    left -= extra;
+  }
+  for (int r = 0; left > 0; r = (r + 1) % R, --left) pieces[r] += 1;
+  for (int r = 0; r < R; ++r)
+    for (int k = 0; k < pieces[r]; ++k)
+      out.push_back({p->rstart[r] + p->rlen[r] * k / pieces[r], p->rstart[r] + p->rlen[r] * (k + 1) / pieces[r]});
+  return out;
+}
+
+// chunk k of ring r clipped to a lane; empty when they do not meet
+std::pair<int64_t, int64_t> clip(std::pair<int64_t, int64_t> chunk, std::pair<int64_t, int64_t> lane) {
+  const int64_t lo = std::max(chunk.first, lane.first), hi = std::min(chunk.second, lane.second);
+  return {lo, std::max(lo, hi)};
+}
+
 // Upper bounds of the push layout, from the schedule alone (before any
 // pointer is known): staging elements per writer slot, unit flags per lane.
 void push_bounds(const rv_plan *p, int64_t *stride_bound, int64_t *units_max) {
   const int es = elem_size(p->dtype);
   const int64_t nmax = 16 / es, unit_elems = kMinUnitBytes / es;
+  const auto lanes = lane_ranges(p);
   int64_t stride = nmax;
   int64_t umax = 1;
-  for (int l = 0; l < p->n_lanes; ++l) {
+  for (const auto &ln : lanes) {
     int64_t u = 0;
-    for (int r = l; r < p->R; r += p->n_lanes) {
-      const int64_t chunk = (p->rlen[r] + p->C - 1) / p->C;
-      u += (chunk + unit_elems - 1) / unit_elems + 1;
+    for (int r = 0; r < p->R; ++r) {
+      const int64_t meet = clip({p->rstart[r], p->rstart[r] + p->rlen[r]}, ln).second -
+                           clip({p->rstart[r], p->rstart[r] + p->rlen[r]}, ln).first;
+      if (meet <= 0) continue;
+      const int64_t piece = std::min(meet, (p->rlen[r] + p->C - 1) / p->C);
+      u += (piece + unit_elems - 1) / unit_elems + 1;
+      stride += piece + 2 * nmax;  // one piece per owner per (ring, lane), padded for alignment
     }
     umax = std::max(umax, u);
   }
-  for (int r = 0; r < p->R; ++r) stride += (p->rlen[r] + p->C - 1) / p->C + 2 * nmax;
   *stride_bound = (stride + 63) / 64 * 64;  // writer slots stay 256-byte aligned
   *units_max = umax;
 }
@@ -192,6 +236,9 @@ int upload(rv_plan::Lane &lane, const std::vector<Seg> &segs, const std::vector<
   }
   return RV_OK;
 }
+
+// lanes (launches / streams per cycle) a plan can hold beyond one per ring
+constexpr int kMaxLanes = 64;
 
 // push: target work items (scatter + fold units) per resident block; more
 // items shrink the tail when blocks finish unevenly, fewer amortise flags
@@ -271,6 +318,7 @@ int build_tables(rv_plan *p) {
 
   free_lanes(p);
   p->lanes.resize(p->n_lanes);
+  const auto ranges = lane_ranges(p);
   std::vector<int> loc = p->local;
   std::sort(loc.begin(), loc.end());
   std::vector<int64_t> cursor(p->C, 0);  // push: staging cursor per owner, across lanes
@@ -279,14 +327,20 @@ int build_tables(rv_plan *p) {
     rv_plan::Lane &lane = p->lanes[l];
     std::vector<Seg> segs;
     std::vector<int64_t> prefix(1, 0);
-    for (int r = l; r < p->R; r += p->n_lanes) lane.rings.push_back(r);
+    lane.lo = ranges[l].first;
+    lane.hi = ranges[l].second;
+    for (int r = 0; r < p->R; ++r) {
+      const auto m = clip({p->rstart[r], p->rstart[r] + p->rlen[r]}, ranges[l]);
+      if (m.second > m.first) lane.rings.push_back(r);
+    }
     if (!push) {
       for (int r : lane.rings) {
         const auto bounds = ring_chunks(p, r);
         for (int k : loc) {
           Seg s{};
-          s.lo = bounds[k].first;
-          s.hi = bounds[k].second;
+          const auto piece = clip(bounds[k], ranges[l]);
+          s.lo = piece.first;
+          s.hi = piece.second;
           s.k = k;
           s.ring = r;
           if (s.hi <= s.lo) continue;
@@ -311,8 +365,9 @@ int build_tables(rv_plan *p) {
         for (int r : lane.rings) {
           const auto bounds = ring_chunks(p, r);
           Seg s{};
-          s.lo = bounds[q].first;
-          s.hi = bounds[q].second;
+          const auto piece = clip(bounds[q], ranges[l]);
+          s.lo = piece.first;
+          s.hi = piece.second;
           s.k = q;
           s.ring = r;
           if (s.hi <= s.lo) continue;
@@ -481,7 +536,7 @@ int rv_plan_create(rv_plan **out, int device, int n_clusters, int n_rings, const
   {
     DeviceGuard g(device);
     cudaError_t e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device);
-    const int lanes_cap = std::max(1, n_rings);
+    const int lanes_cap = std::max(kMaxLanes, n_rings);
     p->flag_bytes = sizeof(unsigned long long) * flag_index(lanes_cap, 0, 0);
     if (e == cudaSuccess) e = cudaMalloc(&p->flags, p->flag_bytes);
     if (e == cudaSuccess) e = cudaMemset(p->flags, 0, p->flag_bytes);
@@ -526,8 +581,8 @@ int rv_plan_set_local(rv_plan *p, const int *positions, int n) {
 
 int rv_plan_set_lanes(rv_plan *p, int n_lanes) {
   if (!p) return set_err(RV_E_ARG, "plan is NULL");
-  if (n_lanes < 1 || n_lanes > std::max(1, p->R))
-    return set_err(RV_E_ARG, "lanes must be in [1, %d]", std::max(1, p->R));
+  if (n_lanes < 1 || n_lanes > std::max(kMaxLanes, p->R))
+    return set_err(RV_E_ARG, "lanes must be in [1, %d]", std::max(kMaxLanes, p->R));
   p->n_lanes = n_lanes;
   p->dirty = true;
   return RV_OK;
@@ -599,7 +654,7 @@ int rv_plan_set_trace(rv_plan *p, int enable) {
   if (!p) return set_err(RV_E_ARG, "plan is NULL");
   DeviceGuard g(p->device);
   if (enable && !p->trace) {
-    const size_t n = 4 * (size_t)std::max(1, p->R);
+    const size_t n = 4 * (size_t)std::max(kMaxLanes, p->R);
     RV_CUDA(cudaMalloc(&p->trace, n * sizeof(unsigned long long)));
     RV_CUDA(cudaMemset(p->trace, 0, n * sizeof(unsigned long long)));
   } else if (!enable && p->trace) {
@@ -612,7 +667,7 @@ int rv_plan_set_trace(rv_plan *p, int enable) {
 int rv_plan_read_trace(rv_plan *p, int lane, uint64_t *out4) {
   if (!p || !out4) return set_err(RV_E_ARG, "NULL argument");
   if (!p->trace) return set_err(RV_E_ARG, "tracing is off");
-  if (lane < 0 || lane >= std::max(1, p->R)) return set_err(RV_E_ARG, "bad lane %d", lane);
+  if (lane < 0 || lane >= std::max(kMaxLanes, p->R)) return set_err(RV_E_ARG, "bad lane %d", lane);
   DeviceGuard g(p->device);
   RV_CUDA(cudaDeviceSynchronize());
   RV_CUDA(cudaMemcpy(out4, p->trace + 4 * lane, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
@@ -666,28 +721,21 @@ int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const 
   }
   for (int l = 0; l < p->n_lanes; ++l) {
     cudaStream_t st = (streams && n_streams > 0) ? (cudaStream_t)streams[l % n_streams] : (cudaStream_t)0;
-    const auto &rings = p->lanes[l].rings;
+    const rv_plan::Lane &lane = p->lanes[l];
+    const size_t off = (size_t)lane.lo * es, bytes = (size_t)(lane.hi - lane.lo) * es;
     if (l > 0) RV_CUDA(cudaStreamWaitEvent(st, p->h2d_done[l - 1], 0));
-    for (size_t i = 0; i < p->local.size(); ++i) {
+    for (size_t i = 0; i < p->local.size() && bytes > 0; ++i) {
       const int pos = p->local[i];
-      for (int r : rings) {
-        if (p->rlen[r] == 0) continue;
-        const size_t off = (size_t)p->rstart[r] * es, bytes = (size_t)p->rlen[r] * es;
-        RV_CUDA(cudaMemcpyAsync((char *)p->src[pos] + off, (const char *)host_src[i] + off, bytes,
-                                cudaMemcpyHostToDevice, st));
-      }
+      RV_CUDA(cudaMemcpyAsync((char *)p->src[pos] + off, (const char *)host_src[i] + off, bytes,
+                              cudaMemcpyHostToDevice, st));
     }
     RV_CUDA(cudaEventRecord(p->h2d_done[l], st));
     int rc = launch_lane(p, l, st);
     if (rc) return rc;
-    for (size_t i = 0; i < p->local.size(); ++i) {
+    for (size_t i = 0; i < p->local.size() && bytes > 0; ++i) {
       const int pos = p->local[i];
-      for (int r : rings) {
-        if (p->rlen[r] == 0) continue;
-        const size_t off = (size_t)p->rstart[r] * es, bytes = (size_t)p->rlen[r] * es;
-        RV_CUDA(cudaMemcpyAsync((char *)host_dst[i] + off, (const char *)p->dst[pos] + off, bytes,
-                                cudaMemcpyDeviceToHost, st));
-      }
+      RV_CUDA(cudaMemcpyAsync((char *)host_dst[i] + off, (const char *)p->dst[pos] + off, bytes,
+                              cudaMemcpyDeviceToHost, st));
     }
   }
   return RV_OK;

@@ -86,6 +86,7 @@ def main():
             ("native", torch.float32, 1, True, False),
             ("f64", torch.float64, 1, False, True),
             ("f64", torch.float32, len(lens), False, False),
+            ("f64", torch.float32, 2 * len(lens) + 1, False, False),
             ("f64", torch.float32, 1, False, True),
         ]
         variants = [v + (proto,) for proto in ("pull", "push") for v in base]

@@ -147,21 +147,51 @@ def test_misaligned_and_ragged(dtype, c):
     assert bits_equal(got, want)
 
 
-def test_lanes_per_ring_match_single_launch():
+@pytest.mark.parametrize("lanes", [2, 4, 7, 16, 64])
+def test_lanes_match_single_launch(lanes):
+    # lanes <= R group whole rings, lanes > R cut rings into pieces
     c = 4
     lens = [100003, 77777, 5, 250001]
     sched = make_sched(lens, c)
     rng = np.random.Generator(np.random.Philox(key=3))
     rows = [rng.normal(0, 1, sched.total_params).astype(np.float32) for _ in range(c)]
     want = np.stack(ring_oracle.ring_mean([r.start for r in sched.rings], lens, rows)).astype(np.float32)
-    ts = {m: torch.from_numpy(r).cuda() for m, r in enumerate(rows)}
-    streams = [torch.cuda.Stream() for _ in lens]
-    cur = torch.cuda.current_stream()
-    for s in streams:
-        s.wait_stream(cur)
-    rv.ring_mean_(sched, ts, lanes=len(lens), streams={0: streams})
-    got = np.stack([ts[m].cpu().numpy() for m in range(c)])
-    assert bits_equal(got, want)
+    for offset in (0, 1):  # TMA path and register path
+        ts, views = {}, []
+        for m, r in enumerate(rows):
+            buf = torch.empty(len(r) + offset, device="cuda")
+            ts[m] = buf[offset:]
+            ts[m].copy_(torch.from_numpy(r))
+        streams = [torch.cuda.Stream() for _ in range(min(lanes, 8))]
+        cur = torch.cuda.current_stream()
+        for s in streams:
+            s.wait_stream(cur)
+        rv.ring_mean_(sched, ts, lanes=lanes, streams={0: streams})
+        got = np.stack([ts[m].cpu().numpy() for m in range(c)])
+        assert bits_equal(got, want), (lanes, offset)
+
+
+def test_host_buffer_pipeline_many_lanes():
+    # rv_allreduce_mean_host with lanes > R: host -> device -> average -> host
+    c = 3
+    lens = [300001, 17, 200003]
+    sched = make_sched(lens, c)
+    rng = np.random.Generator(np.random.Philox(key=8))
+    rows = [rng.normal(0, 1, sched.total_params).astype(np.float32) for _ in range(c)]
+    want = np.stack(ring_oracle.ring_mean([r.start for r in sched.rings], lens, rows)).astype(np.float32)
+    for lanes in (1, 3, 12):
+        g = LocalRingGroup([r.start for r in sched.rings], lens, sched.total_params, [0] * c, torch.float32,
+                           lanes=lanes)
+        dev = [torch.empty(sched.total_params, device="cuda") for _ in range(c)]
+        g.bind_tensors(dev)
+        hin = [torch.from_numpy(r).pin_memory() for r in rows]
+        hout = [torch.empty_like(h).pin_memory() for h in hin]
+        streams = [torch.cuda.Stream() for _ in range(lanes)]
+        g.plans[0].run_host([h.data_ptr() for h in hin], [h.data_ptr() for h in hout], streams)
+        torch.cuda.synchronize()
+        g.check()
+        assert bits_equal(np.stack([h.numpy() for h in hout]), want), lanes
+        g.close()
 
 
 def test_resnet50_size_full_check_against_c_oracle():
