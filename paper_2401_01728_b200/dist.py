@@ -176,7 +176,8 @@ class DistRingGroup:
 
         st = streams if streams is not None else [torch.cuda.current_stream(self.device)]
         st = st if isinstance(st, (list, tuple)) else [st]
-        self.plan.run(st)
+        with torch.cuda.nvtx.range("ravnest_b200.cycle"):
+            self.plan.run(st)
 
     def average_host(self, host_src, host_dst, streams=None) -> None:
         """Cycle from/to pinned HOST tensors: H2D, average, D2H, pipelined
@@ -185,7 +186,8 @@ class DistRingGroup:
 
         st = streams if streams is not None else [torch.cuda.current_stream(self.device)]
         st = st if isinstance(st, (list, tuple)) else [st]
-        self.plan.run_host([host_src.data_ptr()], [host_dst.data_ptr()], st)
+        with torch.cuda.nvtx.range("ravnest_b200.cycle_host"):
+            self.plan.run_host([host_src.data_ptr()], [host_dst.data_ptr()], st)
 
     def check(self) -> None:
         self.plan.check_status()

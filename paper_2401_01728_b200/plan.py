@@ -223,6 +223,12 @@ class LocalRingGroup:
         streams for per-ring lanes); default is torch's current stream."""
         import torch
 
+        with torch.cuda.nvtx.range("ravnest_b200.cycle"):
+            self._run(streams)
+
+    def _run(self, streams) -> None:
+        import torch
+
         for d in self.device_order:
             if streams is not None and d in streams:
                 st = streams[d]
