@@ -126,6 +126,27 @@ def ncu_traffic(workload: str, c: int, n_gpus: int, acc: str):
         return None
 
 
+def bind_to_gpu_numa(device: int) -> str:
+    """Pin this process to the CPUs local to `device`'s PCIe root (sysfs
+    local_cpulist) so pinned host buffers for the e2e leg are allocated on
+    the GPU's own NUMA node.  Returns the cpulist used ('' if unknown)."""
+    import torch
+
+    try:
+        props = torch.cuda.get_device_properties(device)
+        bus = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        os.sched_setaffinity(0, cpus)
+        return spec
+    except Exception:
+        return ""
+
+
 def ring_starts(lens):
     out, s = [], 0
     for n in lens:
@@ -499,6 +520,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     ms, kernel_ms = float(t[0]), float(t[1])
 
     # e2e through the host-buffer C ABI: pinned host -> GPU -> average -> host
+    numa_cpus = bind_to_gpu_numa(local_rank) if args.numa_bind else ""
     hsrc = x.cpu().pin_memory()
     hdst = torch.empty_like(hsrc).pin_memory()
     grp_e2e = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.e2e_lanes,
@@ -566,7 +588,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3) * world, 3), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": world * total * 4, "d2h_bytes_per_step": world * total * 4,
-                    "path": f"rv_allreduce_mean_host (pinned host fp32, {args.e2e_lanes} pipelined lanes)"},
+                    "path": f"rv_allreduce_mean_host (pinned host fp32, {args.e2e_lanes} pipelined lanes)",
+                    "host_cpus_rank0": numa_cpus or None},
             "gpu_launches": args.steps * (args.lanes + (1 if args.blend else 0)) * world,
             "clocks": clk,
         }
@@ -635,6 +658,7 @@ def main():
     ap.add_argument("--blend", type=int, default=0, help="config 4: snapshot average + delayed-update blend")
     ap.add_argument("--tau", type=int, default=4)
     ap.add_argument("--trace", type=int, default=1, help="N>1: add a device-side phase trace")
+    ap.add_argument("--numa-bind", type=int, default=1, help="bind ranks to their GPU's NUMA-local CPUs for e2e")
     ap.add_argument("--e2e-lanes", type=int, default=0,
                     help="pipeline stages of the host-buffer path (0: 16 on one GPU, one per ring across GPUs)")
     args = ap.parse_args()
