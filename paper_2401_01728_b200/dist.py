@@ -174,10 +174,10 @@ class DistRingGroup:
         """Launch one cycle on ``streams`` (default: the current stream)."""
         import torch
 
-        st = streams if streams is not None else [torch.cuda.current_stream(self.device)]
-        st = st if isinstance(st, (list, tuple)) else [st]
-        with torch.cuda.nvtx.range("ravnest_b200.cycle"):
-            self.plan.run(st)
+        if streams is None:
+            self.plan.run((torch.cuda.current_stream(self.device).cuda_stream,))
+            return
+        self.plan.run(streams if isinstance(streams, (list, tuple)) else [streams])
 
     def average_host(self, host_src, host_dst, streams=None) -> None:
         """Cycle from/to pinned HOST tensors: H2D, average, D2H, pipelined

@@ -57,6 +57,8 @@ class DevicePlan:
         N.check(self.lib.rv_plan_create(ctypes.byref(h), self.device, self.n_clusters, len(starts), rs, rl,
                                         int(total), int(dtype_code), ACC_MODES[acc]), "rv_plan_create")
         self._h = h
+        self._launch = self.lib.rv_allreduce_mean
+        self._stream_cache: dict = {}
 
     @property
     def handle(self):
@@ -118,8 +120,13 @@ class DevicePlan:
         N.check(self.lib.rv_plan_set_peers(self._h, int(rank), int(n_ranks), arr), "rv_plan_set_peers")
 
     def run(self, streams: Sequence = (None,)) -> None:
-        hs = [_stream_handle(s) for s in streams] or [0]
-        N.check(self.lib.rv_allreduce_mean(self._h, N.ptr_array(hs), len(hs)), "rv_allreduce_mean")
+        key = tuple(_stream_handle(s) for s in streams) or (0,)
+        arr = self._stream_cache.get(key)
+        if arr is None:  # ctypes arrays are cached: the launch path stays a few microseconds
+            arr = self._stream_cache[key] = N.ptr_array(key)
+        rc = self._launch(self._h, arr, len(key))
+        if rc:
+            N.check(rc, "rv_allreduce_mean")
 
     def run_host(self, host_src: Sequence[int], host_dst: Sequence[int], streams: Sequence = (None,)) -> None:
         hs = [_stream_handle(s) for s in streams] or [0]
