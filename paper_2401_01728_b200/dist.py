@@ -192,8 +192,21 @@ class DistRingGroup:
     def check(self) -> None:
         self.plan.check_status()
 
-    def close(self) -> None:
+    def close(self, barrier: bool = True) -> None:
+        """Release the plan and the peer mappings.  Collective by default:
+        every rank finishes its cycles (device sync) and meets the others
+        before anything is unmapped, so no kernel still touches a peer's
+        buffer or this rank's staging when it goes away."""
+        import torch
+        import torch.distributed as dist
+
+        if self.plan is None:
+            return
+        torch.cuda.synchronize(self.device)
+        if barrier and dist.is_initialized():
+            dist.barrier(group=self.group)
         for p in self._imported:
             _close(self.device, p)
         self._imported = []
         self.plan.close()
+        self.plan = None
