@@ -100,6 +100,11 @@ int rv_plan_set_local(rv_plan *plan, const int *positions, int n_positions);
  * cut rings into equal pieces -- finer host-buffer pipelining. */
 int rv_plan_set_lanes(rv_plan *plan, int n_lanes);
 
+/* The lane partition rv_plan_set_lanes uses (host-only, no device needed):
+ * lane l covers [lane_lo[l], lane_hi[l]). */
+int rv_lane_ranges(int n_rings, const int64_t *ring_start, const int64_t *ring_len, int n_lanes,
+                   int64_t *lane_lo, int64_t *lane_hi);
+
 /* This plan's flag area (device memory, cudaMalloc'd: IPC-exportable). */
 int rv_plan_flag_area(rv_plan *plan, void **flags, size_t *bytes);
 

@@ -46,6 +46,7 @@ SIGNATURES = {
     "rv_plan_bind": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "rv_plan_set_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
     "rv_plan_set_lanes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "rv_lane_ranges": (ctypes.c_int, [ctypes.c_int, _c_i64_p, _c_i64_p, ctypes.c_int, _c_i64_p, _c_i64_p]),
     "rv_plan_flag_area": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, ctypes.POINTER(ctypes.c_size_t)]),
     "rv_plan_set_peers": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _c_void_pp]),
     "rv_plan_set_protocol": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
@@ -116,3 +117,15 @@ def check(rc: int, what: str = "") -> None:
 
 def ptr_array(ptrs) -> ctypes.Array:
     return (ctypes.c_void_p * max(1, len(ptrs)))(*[ctypes.c_void_p(int(p)) for p in ptrs])
+
+
+def lane_ranges(starts, lens, n_lanes: int) -> list[tuple[int, int]]:
+    """The element ranges the C plan assigns to its lanes (rv_lane_ranges)."""
+    lib = load()
+    R = len(lens)
+    rs = (ctypes.c_int64 * max(1, R))(*[int(x) for x in starts])
+    rl = (ctypes.c_int64 * max(1, R))(*[int(x) for x in lens])
+    lo = (ctypes.c_int64 * n_lanes)()
+    hi = (ctypes.c_int64 * n_lanes)()
+    check(lib.rv_lane_ranges(R, rs, rl, int(n_lanes), lo, hi), "rv_lane_ranges")
+    return list(zip(lo, hi))

@@ -674,6 +674,26 @@ int rv_plan_read_trace(rv_plan *p, int lane, uint64_t *out4) {
   return RV_OK;
 }
 
+int rv_lane_ranges(int n_rings, const int64_t *ring_start, const int64_t *ring_len, int n_lanes,
+                   int64_t *lane_lo, int64_t *lane_hi) {
+  if (n_rings < 0 || n_lanes < 1 || n_lanes > std::max(kMaxLanes, n_rings) || !lane_lo || !lane_hi ||
+      (n_rings > 0 && (!ring_start || !ring_len)))
+    return set_err(RV_E_ARG, "bad lane-range arguments");
+  rv_plan q;  // host-only description; no device state is touched
+  q.R = n_rings;
+  q.n_lanes = n_lanes;
+  q.rstart.assign(ring_start, ring_start + n_rings);
+  q.rlen.assign(ring_len, ring_len + n_rings);
+  q.total = 0;
+  for (int r = 0; r < n_rings; ++r) q.total += ring_len[r];
+  const auto ranges = lane_ranges(&q);
+  for (int l = 0; l < n_lanes; ++l) {
+    lane_lo[l] = ranges[l].first;
+    lane_hi[l] = ranges[l].second;
+  }
+  return RV_OK;
+}
+
 int rv_plan_set_max_blocks(rv_plan *p, int max_blocks) {
   if (!p || max_blocks < 0) return set_err(RV_E_ARG, "bad block budget");
   p->max_blocks = max_blocks;

@@ -65,3 +65,32 @@ def test_plan_create_validates_before_touching_cuda():
     rl2 = (ctypes.c_int64 * 1)(9)
     assert lib.rv_plan_create(ctypes.byref(h), 0, 2, 1, rs, rl2, 10, 0, 0) == _native.RV_E_LAYOUT
     assert lib.rv_plan_create(ctypes.byref(h), 0, 2, 1, rs, rl, 10, 7, 0) == _native.RV_E_CONFIG
+
+
+@pytest.mark.parametrize("lens", [[10], [5, 0, 7, 100], [26201088, 27168768, 27170304, 28942080], [3] * 9, [0, 0]])
+@pytest.mark.parametrize("n_lanes", [1, 2, 3, 4, 9, 16, 64])
+def test_lane_partition(lens, n_lanes):
+    # lanes tile [0, total) in order; up to R lanes they are unions of whole
+    # rings (R lanes = one ring each), beyond R they never straddle a ring
+    starts = [sum(lens[:i]) for i in range(len(lens))]
+    total = sum(lens)
+    R = len(lens)
+    if n_lanes > max(64, R):
+        pytest.skip("beyond capacity")
+    got = _native.lane_ranges(starts, lens, n_lanes)
+    assert len(got) == n_lanes
+    cursor = 0
+    for lo, hi in got:
+        assert lo == cursor and hi >= lo
+        cursor = hi
+    assert cursor == total
+    edges = set(starts) | {total}
+    if n_lanes <= R:
+        assert all(lo in edges and hi in edges for lo, hi in got)
+        if n_lanes == R:
+            assert got == [(s, s + n) for s, n in zip(starts, lens)]
+    else:
+        for lo, hi in got:
+            if hi > lo:
+                r = max(i for i, s in enumerate(starts) if s <= lo)
+                assert hi <= starts[r] + lens[r]
