@@ -13,8 +13,8 @@ sustained per-GPU, per-direction NVLink rate of the transport.  ``fit``
 calibrates (alpha, beta) by least squares on relative error from sweep rows
 (tools/sweep.py output); ``CALIBRATED`` holds the values fitted on
 profiles/r01/sweep_n4_current.jsonl (4 x B200, 24 shard-size x ring-count
-points from 1 MiB to 8 GiB per cluster; max relative error 10 % for pull,
-13.5 % for push, under 3 % above 32 MiB per cluster).
+points from 1 MiB to 8 GiB per cluster; max relative error 8 % for pull,
+16 % for push, under 4 % above 32 MiB per cluster).
 """
 
 from __future__ import annotations
@@ -35,8 +35,8 @@ class NvlinkModel:
 
 
 CALIBRATED = {
-    "pull": NvlinkModel(27.89e-6, 644.6e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs)"),
-    "push": NvlinkModel(31.97e-6, 682.4e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs, adaptive units)"),
+    "pull": NvlinkModel(27.82e-6, 642.0e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs)"),
+    "push": NvlinkModel(30.77e-6, 677.4e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs, adaptive units)"),
     "nccl": NvlinkModel(3.16e-6, 606.2e9, "profiles/r01/sweep_n4.jsonl; + 23.3 us per ring call"),
 }
 
