@@ -68,9 +68,14 @@ extern "C" {
  * RV_PROTO_PUSH: NVLink carries stores only -- each member stores its copy of
  *   chunk k into owner k's staging slot (one release flag per 256 KB unit),
  *   the owner folds from local memory and stores the mean into every member
- *   (depart barrier only).  Needs one position per rank, rank == position. */
+ *   (depart barrier only).  Needs one position per rank, rank == position.
+ * RV_PROTO_LL: latency transport for small fp32 sets -- every 16-byte store
+ *   carries two values each tagged with the cycle's epoch, readers poll the
+ *   data itself: no fences, no flags, no barriers; twice the NVLink bytes.
+ *   Same placement rule as push; its area comes from rv_plan_push_area. */
 #define RV_PROTO_PULL 0
 #define RV_PROTO_PUSH 1
+#define RV_PROTO_LL 2
 
 typedef struct rv_plan rv_plan;
 

@@ -29,6 +29,7 @@ RV_ACC_NATIVE = 1
 
 RV_PROTO_PULL = 0
 RV_PROTO_PUSH = 1
+RV_PROTO_LL = 2
 
 RV_MAX_CLUSTERS = 16
 RV_MAX_RANKS = 16

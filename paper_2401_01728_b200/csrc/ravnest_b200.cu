@@ -161,7 +161,10 @@ void set_body(Seg &s, int N, int64_t a0) {
   s.body_hi = bhi;
 }
 
-bool push_active(const rv_plan *p) { return p->proto == RV_PROTO_PUSH && p->n_ranks > 1; }
+bool push_active(const rv_plan *p) {
+  return (p->proto == RV_PROTO_PUSH || p->proto == RV_PROTO_LL) && p->n_ranks > 1;
+}
+bool ll_active(const rv_plan *p) { return p->proto == RV_PROTO_LL && p->n_ranks > 1; }
 
 // Lane l is the element range [first, second) of the parameter vector that
 // one launch (on its own stream) averages.  n_lanes <= R: consecutive whole
@@ -206,7 +209,8 @@ std::pair<int64_t, int64_t> clip(std::pair<int64_t, int64_t> chunk, std::pair<in
 // pointer is known): staging elements per writer slot, unit flags per lane.
 void push_bounds(const rv_plan *p, int64_t *stride_bound, int64_t *units_max) {
   const int es = elem_size(p->dtype);
-  const int64_t nmax = 16 / es, unit_elems = kMinUnitBytes / es;
+  const bool ll = p->proto == RV_PROTO_LL;
+  const int64_t nmax = ll ? 2 : 16 / es, unit_elems = ll ? kLLUnit : kMinUnitBytes / es;
   const auto lanes = lane_ranges(p);
   int64_t stride = nmax;
   int64_t umax = 1;
@@ -273,13 +277,20 @@ int build_tables(rv_plan *p) {
       if (!p->peer_push[r]) return set_err(RV_E_ARG, "push area of rank %d missing", r);
   }
   p->use_push = push;
+  const bool ll = ll_active(p);
+  if (ll && p->dtype != RV_DTYPE_F32) return set_err(RV_E_CONFIG, "the LL transport carries fp32 parameters only");
   const int mode = p->dtype == RV_DTYPE_F64 ? kF64 : (p->acc == RV_ACC_NATIVE ? kF32Native : kF32Acc64);
   int U = 1;
   int64_t tile_vecs = 0;
   DeviceGuard g(p->device);
   const char *tma_env = getenv("RAVNEST_B200_TMA");
   const bool tma = vec && p->n_ranks == 1 && !(tma_env && tma_env[0] == '0');
-  if (tma) {
+  if (ll) {
+    p->kernel = pick_ll_kernel(mode, p->C);
+    p->block_threads = kThreads;
+    p->smem_bytes = 0;
+    tile_vecs = kLLUnit;
+  } else if (tma) {
     int tv = 0;
     p->kernel = pick_tma_kernel(mode, p->C, &tv, &p->smem_bytes);
     p->block_threads = kTmaConsumers + 32;
@@ -298,7 +309,7 @@ int build_tables(rv_plan *p) {
   // it depends only on the schedule and the device model, so every rank
   // derives the same layout
   int64_t unit_vecs = kUnitBytes / (N * es);
-  if (push) {
+  if (push && !ll) {
     int64_t owner_elems = 0;
     for (int q = 0; q < p->C; ++q) {
       int64_t e = 0;
@@ -372,14 +383,22 @@ int build_tables(rv_plan *p) {
           s.ring = r;
           if (s.hi <= s.lo) continue;
           set_body(s, N, a0);
-          // staging index of element i is stage_off + (i - lo); keep it
-          // vector-aligned exactly where the source is
-          const int64_t c0 = (cursor[q] + N - 1) / N * N;
-          s.stage_off = c0 + ((s.lo + a0) % N);
-          cursor[q] = s.stage_off + (s.hi - s.lo);
           s.unit0 = u;
-          const int64_t nvec = (s.body_hi - s.body_lo) / N;
-          u += std::max<int64_t>(1, (nvec + unit_vecs - 1) / unit_vecs);
+          if (ll) {
+            // LL words pair up elements: even offsets keep each pair in one
+            // 16-byte {v0, e, v1, e} store
+            s.stage_off = (cursor[q] + 1) / 2 * 2;
+            cursor[q] = s.stage_off + (s.hi - s.lo);
+            u += (s.hi - s.lo + kLLUnit - 1) / kLLUnit;
+          } else {
+            // staging index of element i is stage_off + (i - lo); keep it
+            // vector-aligned exactly where the source is
+            const int64_t c0 = (cursor[q] + N - 1) / N * N;
+            s.stage_off = c0 + ((s.lo + a0) % N);
+            cursor[q] = s.stage_off + (s.hi - s.lo);
+            const int64_t nvec = (s.body_hi - s.body_lo) / N;
+            u += std::max<int64_t>(1, (nvec + unit_vecs - 1) / unit_vecs);
+          }
           segs.push_back(s);
           if (q == p->rank) lane.elems += s.hi - s.lo;
         }
@@ -393,7 +412,7 @@ int build_tables(rv_plan *p) {
       for (int q = 0; q < p->C; ++q)
         if (q != p->rank) lane.scatter_umax = std::max(lane.scatter_umax, lane.ounits[q]);
       lane.nseg = (int)segs.size();
-      lane.n_tiles = (int64_t)(p->C - 1) * lane.scatter_umax + lane.ounits[p->rank];
+      lane.n_tiles = (int64_t)(p->C - 1) * lane.scatter_umax * (ll ? 2 : 1) + lane.ounits[p->rank];
       int rc = upload(lane, segs, {});
       if (rc) return rc;
     }
@@ -612,7 +631,8 @@ int rv_plan_set_peers(rv_plan *p, int rank, int n_ranks, void *const *areas) {
 
 int rv_plan_set_protocol(rv_plan *p, int proto) {
   if (!p) return set_err(RV_E_ARG, "plan is NULL");
-  if (proto != RV_PROTO_PULL && proto != RV_PROTO_PUSH) return set_err(RV_E_CONFIG, "unknown protocol %d", proto);
+  if (proto != RV_PROTO_PULL && proto != RV_PROTO_PUSH && proto != RV_PROTO_LL)
+    return set_err(RV_E_CONFIG, "unknown protocol %d", proto);
   p->proto = proto;
   p->dirty = true;
   return RV_OK;
@@ -627,12 +647,18 @@ int rv_plan_push_area(rv_plan *p, void **area, size_t *bytes) {
   }
   if (!p->push_area) {
     push_bounds(p, &p->stride_bound, &p->units_max);
-    const size_t nflags = (size_t)std::max(1, p->n_lanes) * p->C * p->units_max;
-    p->pflag_bytes = (nflags * sizeof(unsigned long long) + 4095) / 4096 * 4096;
-    p->push_bytes = p->pflag_bytes + (size_t)p->C * p->stride_bound * elem_size(p->dtype);
+    if (p->proto == RV_PROTO_LL) {
+      // [staging: C writer slots | receive: C owner slots], 8 bytes per element
+      p->pflag_bytes = 0;
+      p->push_bytes = 2 * (size_t)p->C * p->stride_bound * 8;
+    } else {
+      const size_t nflags = (size_t)std::max(1, p->n_lanes) * p->C * p->units_max;
+      p->pflag_bytes = (nflags * sizeof(unsigned long long) + 4095) / 4096 * 4096;
+      p->push_bytes = p->pflag_bytes + (size_t)p->C * p->stride_bound * elem_size(p->dtype);
+    }
     DeviceGuard g(p->device);
     RV_CUDA(cudaMalloc(&p->push_area, p->push_bytes));
-    RV_CUDA(cudaMemset(p->push_area, 0, p->pflag_bytes));
+    RV_CUDA(cudaMemset(p->push_area, 0, p->proto == RV_PROTO_LL ? p->push_bytes : p->pflag_bytes));
     RV_CUDA(cudaDeviceSynchronize());
     p->push_lanes = p->n_lanes;
     p->dirty = true;

@@ -107,3 +107,16 @@ KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
     default: return vec ? pick_cb<double, double, 16>(c, push, u_out) : pick_cb<double, double, 8>(c, push, u_out);
   }
 }
+
+// LL transport (fp32 storage only)
+template <typename Acc>
+KernelFn pick_ll(int c) {
+  if (c <= 2) return ring_ll_kernel<Acc, 2>;
+  if (c <= 4) return ring_ll_kernel<Acc, 4>;
+  if (c <= 8) return ring_ll_kernel<Acc, 8>;
+  return ring_ll_kernel<Acc, 16>;
+}
+
+KernelFn pick_ll_kernel(int mode, int c) {
+  return mode == kF32Native ? pick_ll<float>(c) : pick_ll<double>(c);
+}

@@ -184,6 +184,163 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// LL transport (small fp32 sets; one position per rank, rank == position):
+// latency instead of bandwidth.  Every 16-byte store carries two fp32 values
+// each paired with the cycle's epoch as a flag ({v0, e, v1, e}); readers poll
+// the data itself, so there are no fences, no unit flags and no barriers:
+//   scatter  member -> owner q's LL staging slot (chunk q of every ring)
+//   fold     owner waits for every member's words, folds in ring order,
+//            divides, writes its own buffer and LL words into every
+//            member's receive area
+//   receive  member waits for the owners' words and writes its buffer.
+// All words a rank receives in a cycle are consumed inside that cycle's
+// kernel, and a peer can only start cycle e+1 after it received this rank's
+// cycle-e means, so the areas are reused without resets (epochs differ).
+// Pays twice the bytes on NVLink (8 bytes per value); used below 4 MiB.
+
+constexpr int64_t kLLUnit = 2 * kThreads;  // elements per LL work unit (one pair per thread)
+
+__device__ __forceinline__ void ll_store(unsigned *addr, float v0, float v1, unsigned e) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "r"(__float_as_uint(v0)), "r"(e),
+               "r"(__float_as_uint(v1)), "r"(e)
+               : "memory");
+}
+
+// Spin until both flags of the LL word pair equal e; false on timeout.
+__device__ __forceinline__ bool ll_load(const CycleParams &p, const unsigned *addr, unsigned e, float *v0, float *v1,
+                                        unsigned diag) {
+  unsigned a, b, c, d, spins = 0;
+  unsigned long long t0 = 0;
+  for (;;) {
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(addr)
+                 : "memory");
+    if (b == e && d == e) break;
+    if ((++spins & 1023u) == 0) {
+      if (t0 == 0) t0 = globaltimer();
+      if (*(volatile unsigned *)p.status != 0) return false;
+      if (globaltimer() - t0 > p.timeout_ns) {
+        if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u) p.status[1] = diag;
+        return false;
+      }
+    }
+  }
+  *v0 = __uint_as_float(a);
+  *v1 = __uint_as_float(c);
+  return true;
+}
+
+template <typename Acc, int CB>
+__global__ void __launch_bounds__(kThreads, 2)
+ring_ll_kernel(const __grid_constant__ CycleParams p) {
+  __shared__ int s_ok;
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) {
+    trace_min(p, 0);
+    trace_max(p, 1);
+    s_epoch = *(volatile unsigned long long *)&p.state->epoch + 1ull;
+    s_ok = (*(volatile unsigned *)p.status == 0);
+  }
+  __syncthreads();
+  const unsigned e = (unsigned)s_epoch;
+  const int C = p.C, me = p.me;
+  const float *src = static_cast<const float *>(p.src[me]);
+  float *dst = static_cast<float *>(p.dst[me]);
+  const int64_t n_side = (int64_t)(C - 1) * p.scatter_umax;
+  const int64_t n_work = 2 * n_side + p.ounits[me];
+  bool ok = s_ok;
+
+  for (int64_t w = blockIdx.x; ok && w < n_work; w += gridDim.x) {
+    if (w < n_side || w >= n_side + p.ounits[me]) {
+      // scatter (first range) or receive (last range): unit u of owner q != me
+      const bool scatter = w < n_side;
+      const int64_t v = scatter ? w : w - n_side - p.ounits[me];
+      const int r = (int)(v % (C - 1));
+      const int64_t u = v / (C - 1);
+      int q = me + 1 + r;
+      if (q >= C) q -= C;
+      if (u >= p.ounits[q]) continue;
+      const Seg s = find_unit<float>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
+      const int64_t i0 = s.lo + (u - s.unit0) * kLLUnit + 2 * (int64_t)threadIdx.x;
+      if (i0 >= s.hi || i0 >= s.lo + (u - s.unit0 + 1) * kLLUnit) continue;
+      const bool two = i0 + 1 < s.hi;
+      const int64_t word = s.stage_off + (i0 - s.lo);  // even
+      if (scatter) {
+        unsigned *stage = static_cast<unsigned *>(p.stage[q]);
+        ll_store(stage + 2 * ((int64_t)me * p.stride + word), src[i0], two ? src[i0 + 1] : 0.f, e);
+      } else {
+        const unsigned *recv = static_cast<const unsigned *>(p.stage[me]) + 2 * (int64_t)C * p.stride;
+        float v0, v1;
+        const unsigned diag = (3u << 16) | ((unsigned)p.lane << 8) | (unsigned)q;
+        if (!ll_load(p, recv + 2 * ((int64_t)q * p.stride + word), e, &v0, &v1, diag)) {
+          ok = false;
+          continue;
+        }
+        dst[i0] = v0;
+        if (two) dst[i0 + 1] = v1;
+      }
+    } else {
+      // fold: unit u of this rank's own chunk
+      const int64_t u = w - n_side;
+      const Seg s = find_unit<float>(p.segs + p.oseg_base[me], p.oseg_base[me + 1] - p.oseg_base[me], u);
+      const int64_t i0 = s.lo + (u - s.unit0) * kLLUnit + 2 * (int64_t)threadIdx.x;
+      if (i0 >= s.hi || i0 >= s.lo + (u - s.unit0 + 1) * kLLUnit) continue;
+      const bool two = i0 + 1 < s.hi;
+      const int64_t word = s.stage_off + (i0 - s.lo);
+      const unsigned *stage = static_cast<const unsigned *>(p.stage[me]);
+      Acc a0 = 0, a1 = 0;
+      int m = s.k;  // == me: the fold starts at the owner
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (j < C) {
+          float v0, v1;
+          if (m == me) {
+            v0 = src[i0];
+            v1 = two ? src[i0 + 1] : 0.f;
+          } else {
+            const unsigned diag = (2u << 16) | ((unsigned)p.lane << 8) | (unsigned)m;
+            if (!ll_load(p, stage + 2 * ((int64_t)m * p.stride + word), e, &v0, &v1, diag)) {
+              ok = false;
+              break;
+            }
+          }
+          if (j == 0) {
+            a0 = (Acc)v0;
+            a1 = (Acc)v1;
+          } else {
+            a0 = a0 + (Acc)v0;
+            a1 = a1 + (Acc)v1;
+          }
+          m = (m + 1 == C) ? 0 : m + 1;
+        }
+      }
+      if (!ok) continue;
+      const float m0 = finish<float, Acc>(a0, p), m1 = finish<float, Acc>(a1, p);
+      dst[i0] = m0;
+      if (two) dst[i0 + 1] = m1;
+      for (int q = 0; q < C; ++q) {
+        if (q == me) continue;
+        unsigned *recv = static_cast<unsigned *>(p.stage[q]) + 2 * (int64_t)C * p.stride;
+        ll_store(recv + 2 * ((int64_t)me * p.stride + word), m0, m1, e);
+      }
+    }
+  }
+  if (!ok && threadIdx.x == 0) s_ok = 0;
+  // local bookkeeping only: the last block advances this lane's epoch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    trace_max(p, 2);
+    __threadfence();
+    const unsigned prev = atomicAdd(&p.state->done, 1u);
+    if (prev == gridDim.x - 1) {
+      trace_max(p, 3);
+      p.state->done = 0u;
+      *(volatile unsigned long long *)&p.state->epoch = s_epoch;
+      __threadfence();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // co-resident TMA path (all C members on this device, 16-byte congruent
 // buffers): HBM-bound, so tiles stream through shared memory with bulk async
 // copies.  Warp 0 / lane 0 produces: for each tile it loads the tile of all C

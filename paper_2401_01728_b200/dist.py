@@ -45,17 +45,20 @@ def _close(device: int, ptr: int) -> None:
 
 
 PUSH_MIN_BYTES = 32 << 20
+LL_MAX_BYTES = 4 << 20
 
 
-def choose_protocol(protocol: str, bytes_per_cluster: int) -> str:
-    """'auto': store-only push above 32 MiB per cluster (its per-unit flags
-    pay off and NVLink stores outrun loads: sweep_n4.jsonl), pull below (one
-    kernel round trip, no staging).  Depends only on the schedule and dtype,
-    so every rank picks the same protocol."""
+def choose_protocol(protocol: str, bytes_per_cluster: int, fp32: bool = True) -> str:
+    """'auto': the LL transport for fp32 sets up to 4 MiB per cluster
+    (latency-bound: no fences or barriers), store-only push from 32 MiB (its
+    per-unit flags pay off and NVLink stores outrun loads), pull in between.
+    Depends only on the schedule and dtype, so every rank picks the same."""
     if protocol == "auto":
+        if fp32 and bytes_per_cluster <= LL_MAX_BYTES:
+            return "ll"
         return "push" if bytes_per_cluster >= PUSH_MIN_BYTES else "pull"
-    if protocol not in ("pull", "push"):
-        raise ConfigError(f"unknown protocol {protocol!r} (auto, pull or push)")
+    if protocol not in ("pull", "push", "ll"):
+        raise ConfigError(f"unknown protocol {protocol!r} (auto, pull, push or ll)")
     return protocol
 
 
@@ -130,7 +133,7 @@ class DistRingGroup:
             self.plan.set_timeout(timeout_s)
         if max_blocks:
             self.plan.set_max_blocks(max_blocks)
-        protocol = choose_protocol(protocol, total * src.element_size())
+        protocol = choose_protocol(protocol, total * src.element_size(), src.element_size() == 4)
         self.protocol = protocol
         self.plan.set_protocol(protocol)
         flag_ptr, _ = self.plan.flag_area()
@@ -141,7 +144,7 @@ class DistRingGroup:
             "flags": _export(flag_ptr),
         }
         push_ptr = 0
-        if protocol == "push":
+        if protocol in ("push", "ll"):
             push_ptr, _ = self.plan.push_area()
             mine["push"] = _export(push_ptr)
         everyone, order, self.position = rendezvous(mine, group)
@@ -159,14 +162,14 @@ class DistRingGroup:
             d = s if e["dst"] == e["src"] else _import(self.device, *e["dst"])
             f = _import(self.device, *e["flags"])
             self._imported += [s, f] + ([d] if d != s else [])
-            if protocol == "push":
+            if protocol in ("push", "ll"):
                 push_areas[pos] = _import(self.device, *e["push"])
                 self._imported.append(push_areas[pos])
             self.plan.bind(pos, s, d)
             areas[pos] = f
         self.plan.set_local([self.position])
         self.plan.set_peers(self.position, self.world, areas)
-        if protocol == "push":
+        if protocol in ("push", "ll"):
             self.plan.set_push_peers(push_areas)
         dist.barrier(group=group)
 

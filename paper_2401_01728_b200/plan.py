@@ -20,7 +20,7 @@ from . import _native as N
 from .errors import ConfigError, LayoutError
 
 ACC_MODES = {"f64": N.RV_ACC_F64, "native": N.RV_ACC_NATIVE}
-PROTOCOLS = {"pull": N.RV_PROTO_PULL, "push": N.RV_PROTO_PUSH}
+PROTOCOLS = {"pull": N.RV_PROTO_PULL, "push": N.RV_PROTO_PUSH, "ll": N.RV_PROTO_LL}
 
 
 def _dtype_code(dtype) -> int:
@@ -78,7 +78,7 @@ class DevicePlan:
 
     def set_protocol(self, proto: str) -> None:
         if proto not in PROTOCOLS:
-            raise ConfigError(f"unknown protocol {proto!r} (use 'pull' or 'push')")
+            raise ConfigError(f"unknown protocol {proto!r} (use 'pull', 'push' or 'll')")
         N.check(self.lib.rv_plan_set_protocol(self._h, PROTOCOLS[proto]), "rv_plan_set_protocol")
 
     def push_area(self) -> tuple[int, int]:
@@ -197,13 +197,13 @@ class LocalRingGroup:
             for rank, d in enumerate(self.device_order):
                 self.plans[d].set_peers(rank, len(self.device_order), areas)
         self.protocol = protocol if len(self.device_order) > 1 else "pull"
-        if self.protocol == "push":
-            # store-only transport: one cluster per device, position == rank
+        if self.protocol in ("push", "ll"):
+            # owner-staged transports: one cluster per device, position == rank
             if sorted(self.devices) != self.devices or len(set(self.devices)) != len(self.devices):
-                raise ConfigError("push needs one cluster per device, in device order")
+                raise ConfigError(f"{self.protocol} needs one cluster per device, in device order")
             push = []
             for d in self.device_order:
-                self.plans[d].set_protocol("push")
+                self.plans[d].set_protocol(self.protocol)
                 push.append(self.plans[d].push_area()[0])
             for d in self.device_order:
                 self.plans[d].set_push_peers(push)

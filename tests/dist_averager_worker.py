@@ -34,7 +34,8 @@ def main():
     n = sum(lens)
     eta = 1e-2
     failures = 0
-    for kappa, tau, graph, proto in ((3, 0, False, "pull"), (4, 2, False, "push"), (5, 3, True, "auto")):
+    for kappa, tau, graph, proto in ((3, 0, False, "pull"), (4, 2, False, "push"), (5, 3, True, "auto"),
+                                     (2, 1, True, "ll")):
         init = [torch.randn(n, device=dev, generator=torch.Generator(device=dev).manual_seed(7 + m))
                 for m in range(world)]
         live = init[rank].clone()

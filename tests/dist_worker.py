@@ -30,7 +30,7 @@ def stall_phase(rank, world, local):
     failures = 0
     lens = [4097, 333]
     total = sum(lens)
-    for proto in ("pull", "push"):
+    for proto in ("pull", "push", "ll"):
         x = torch.full((total,), float(rank), device=f"cuda:{local}")
         g = DistRingGroup(src=x, starts=[0, lens[0]], lens=lens, protocol=proto, timeout_s=0.5)
         if rank == 0:
@@ -89,7 +89,8 @@ def main():
             ("f64", torch.float32, 2 * len(lens) + 1, False, False),
             ("f64", torch.float32, 1, False, True),
         ]
-        variants = [v + (proto,) for proto in ("pull", "push") for v in base]
+        variants = [v + (proto,) for proto in ("pull", "push", "ll") for v in base
+                    if not (proto == "ll" and v[1] == torch.float64)]
         for acc, dt, lanes, reverse_ids, src_ne_dst, proto in variants:
             npdt = np.float32 if dt == torch.float32 else np.float64
             xs = [np.random.Generator(np.random.Philox(key=1000 * ci + m)).normal(0, 1, total).astype(npdt)

@@ -309,17 +309,21 @@ def test_local_group_across_devices():
         rv.ring_mean_(sched, ts)
         got = np.stack([ts[m].cpu().numpy() for m in range(c)])
         assert bits_equal(got, want)
-        # the store-only transport in one process
-        g = LocalRingGroup([r.start for r in sched.rings], lens, sched.total_params, list(range(c)),
-                           torch.float32, protocol="push")
-        ts = [torch.from_numpy(rows[m]).to(f"cuda:{m}") for m in range(c)]
-        g.bind_tensors(ts)
-        g.run()
-        for m in range(c):
-            torch.cuda.synchronize(m)
-        g.check()
-        assert bits_equal(np.stack([t.cpu().numpy() for t in ts]), want)
-        g.close()
+        # the store-only and LL transports in one process
+        for proto in ("push", "ll"):
+            g = LocalRingGroup([r.start for r in sched.rings], lens, sched.total_params, list(range(c)),
+                               torch.float32, protocol=proto)
+            ts = [torch.from_numpy(rows[m]).to(f"cuda:{m}") for m in range(c)]
+            g.bind_tensors(ts)
+            for _ in range(3):  # repeated cycles: epochs advance, areas reused
+                for m in range(c):
+                    ts[m].copy_(torch.from_numpy(rows[m]))
+                g.run()
+                for m in range(c):
+                    torch.cuda.synchronize(m)
+                g.check()
+                assert bits_equal(np.stack([t.cpu().numpy() for t in ts]), want), proto
+            g.close()
 
 
 def test_config1_reference_plan_end_to_end():
