@@ -34,7 +34,7 @@ def main():
     z = torch.zeros(1, device="cuda")
     out["torch_add_us"] = timed(lambda: z.add_(1.0), 2000)
     for n in (1024, 1 << 18):
-        for proto in ("pull", "push"):
+        for proto in ("pull", "push", "ll"):
             x = torch.randn(n, device="cuda")
             g = DistRingGroup(src=x, starts=[0], lens=[n], protocol=proto)
             for _ in range(10):

@@ -65,7 +65,8 @@ def main():
             x = torch.randn(total, device="cuda") * 0.02
             row = {"n_gpus": world, "shard_mib": mib, "rings": r, "bytes_per_cluster": total * 4}
             with torch.cuda.stream(stream):
-                for proto in ("pull", "push"):
+                protos = ("pull", "push", "ll") if total * 4 <= (16 << 20) else ("pull", "push")
+                for proto in protos:
                     g = DistRingGroup(src=x, starts=starts, lens=lens, protocol=proto)
                     for _ in range(3):
                         g.average([stream])
