@@ -40,7 +40,7 @@ def cmd_allreduce_bench(args) -> int:
         "reference_model": {"critical_s": ref.critical_seconds, "single_ring_s": ref.single_ring_seconds,
                             "assumes": f"independent links of {args.bandwidth:.3g} B/s per ring"},
     }
-    for proto in ("pull", "push", "nccl"):
+    for proto in ("ll", "pull", "push", "nccl"):
         m = cost.CALIBRATED[proto]
         t = m.cycle_seconds(sched.total_params * 4.0, c)
         if proto == "nccl":

@@ -37,6 +37,7 @@ class NvlinkModel:
 CALIBRATED = {
     "pull": NvlinkModel(27.82e-6, 642.0e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs)"),
     "push": NvlinkModel(30.77e-6, 677.4e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs, adaptive units)"),
+    "ll": NvlinkModel(10.09e-6, 297.4e9, "profiles/r01/sweep_n4_small_ll.jsonl (4 GPUs, <= 4 MiB per cluster)"),
     "nccl": NvlinkModel(3.16e-6, 606.2e9, "profiles/r01/sweep_n4.jsonl; + 23.3 us per ring call"),
 }
 
