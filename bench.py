@@ -387,6 +387,8 @@ def run_single(args):
     total_ms = t_start.elapsed_time(t_end)
     ms = total_ms / args.steps
     kernel_ms = statistics.mean(a.elapsed_time(m) for a, m, _ in evs)
+    per_step = [a.elapsed_time(b) for a, _, b in evs]
+    step_median, step_min = statistics.median(per_step), min(per_step)
 
     # e2e: host (pinned) buffers -> device -> average -> host, via the C ABI
     hsrc = [x.cpu().pin_memory() for x in xs]
@@ -436,6 +438,7 @@ def run_single(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "ms_per_round": round(ms / (2 * (c - 1)), 5),
         "avg_kernel_ms": round(kernel_ms, 4),
+        "ms_per_step_median": round(step_median, 4), "ms_per_step_min": round(step_min, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
         "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
@@ -515,9 +518,10 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     grp.check()
     ms_local = a.elapsed_time(b) / args.steps
     kern_local = statistics.mean(ea.elapsed_time(em) for ea, em, _ in evs)
-    t = torch.tensor([ms_local, kern_local], dtype=torch.float64)
+    per_step = [ea.elapsed_time(eb) for ea, _, eb in evs]
+    t = torch.tensor([ms_local, kern_local, statistics.median(per_step), min(per_step)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # gloo, outside the timed region
-    ms, kernel_ms = float(t[0]), float(t[1])
+    ms, kernel_ms, step_median, step_min = (float(v) for v in t)
 
     # e2e through the host-buffer C ABI: pinned host -> GPU -> average -> host
     numa_cpus = bind_to_gpu_numa(local_rank) if args.numa_bind else ""
@@ -568,6 +572,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "ms_per_round": round(ms / (2 * (c - 1)), 5),
             "avg_kernel_ms": round(kernel_ms, 4),
+            "ms_per_step_median": round(step_median, 4), "ms_per_step_min": round(step_min, 4),
             "bus_gbps_per_gpu": round(bw, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
