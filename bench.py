@@ -322,13 +322,49 @@ def stale_live(snap, key: int, tau: int, eta: float = 1e-3):
     return live
 
 
-def time_steps(fn, stream, steps: int):
+L2_BYTES = 126 * 1024 * 1024  # B200 L2
+
+
+class L2Flush:
+    """Between timed steps, overwrite a buffer twice the L2 size so that no
+    step starts with its inputs cached.  Used when the per-GPU input set does
+    not exceed L2 by itself (ResNet-50 at one cluster per GPU); the flush runs
+    outside each step's events."""
+
+    def __init__(self, device):
+        import torch
+
+        self.buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=device)
+        self.n = 0
+
+    def __call__(self, stream):
+        import torch
+
+        with torch.cuda.stream(stream):
+            self.n += 1
+            self.buf.fill_(float(self.n))
+
+
+def l2_policy(mode: str, input_bytes: int, device):
+    """(flusher or None, config text) for the per-GPU input bytes of a step."""
+    big = input_bytes > 2 * L2_BYTES
+    if mode == "off" or (mode == "auto" and big):
+        return None, f"inputs larger than L2 ({input_bytes / 1e6:.0f} MB per GPU vs {L2_BYTES / 1e6:.0f} MB L2)"
+    return L2Flush(device), (f"L2 flushed before every timed step ({2 * L2_BYTES / 1e6:.0f} MB write, outside the "
+                             f"step's events; inputs {input_bytes / 1e6:.0f} MB per GPU); ms_per_step = mean of the "
+                             f"per-step event intervals")
+
+
+def time_steps(fn, stream, steps: int, flush=None):
     """Per-step CUDA events on `stream`: (start, after-averaging, end).  The
-    first interval is the averaging launch(es) alone -- the roofline basis."""
+    first interval is the averaging launch(es) alone -- the roofline basis.
+    With `flush`, the L2 flush runs before each step's start event."""
     import torch
 
     evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(steps)]
     for a, m, b in evs:
+        if flush is not None:
+            flush(stream)
         a.record(stream)
         fn(m)
         b.record(stream)
@@ -378,16 +414,17 @@ def run_single(args):
     g.check()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    flush, l2_text = l2_policy(args.l2_flush, c * total * 4, dev)
     t_start.record(stream)
-    evs = time_steps(step, stream, args.steps)
+    evs = time_steps(step, stream, args.steps, flush)
     t_end.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     g.check()
     total_ms = t_start.elapsed_time(t_end)
-    ms = total_ms / args.steps
     kernel_ms = statistics.mean(a.elapsed_time(m) for a, m, _ in evs)
     per_step = [a.elapsed_time(b) for a, _, b in evs]
+    ms = total_ms / args.steps if flush is None else statistics.mean(per_step)
     step_median, step_min = statistics.median(per_step), min(per_step)
 
     # e2e: host (pinned) buffers -> device -> average -> host, via the C ABI
@@ -445,7 +482,7 @@ def run_single(args):
         "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                    "placement": "co-resident on cuda:0", "lanes": args.lanes, "parallelism": "replicas only",
                    "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
-                   "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
+                   "l2": l2_text},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4),
                      "traffic": ncu_traffic(args.workload, c, 1, args.acc) if not args.blend else None,
@@ -509,16 +546,17 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
+    flush, l2_text = l2_policy(args.l2_flush, total * 4 * (3 if args.blend else 1), dev)
     a.record(stream)
-    evs = time_steps(step, stream, args.steps)
+    evs = time_steps(step, stream, args.steps, flush)
     b.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop() if clocks else None
     grp.check()
-    ms_local = a.elapsed_time(b) / args.steps
     kern_local = statistics.mean(ea.elapsed_time(em) for ea, em, _ in evs)
     per_step = [ea.elapsed_time(eb) for ea, _, eb in evs]
+    ms_local = a.elapsed_time(b) / args.steps if flush is None else statistics.mean(per_step)
     t = torch.tensor([ms_local, kern_local, statistics.median(per_step), min(per_step)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # gloo, outside the timed region
     ms, kernel_ms, step_median, step_min = (float(v) for v in t)
@@ -560,7 +598,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
         phases = optional_leg("trace", lambda: trace_phases(grp, step))
     nccl = None
     if args.nccl:
-        nccl = optional_leg("nccl_compare", lambda: nccl_compare(lens, x, world, min(args.steps, 20)))
+        nccl = optional_leg("nccl_compare", lambda: nccl_compare(lens, x, world, min(args.steps, 20), flush))
 
     if rank == 0:
         c = world
@@ -582,7 +620,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
                        "max_blocks": args.max_blocks or None,
                        "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
                        "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
-                       "l2": f"inputs larger than L2 ({total * 4 / 1e6:.0f} MB per cluster)"},
+                       "l2": l2_text},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
                          "traffic": ncu_traffic(args.workload, c, world, args.acc) if grp.protocol == "push" else None,
@@ -636,13 +674,13 @@ def trace_phases(grp, step):
     return {k: round(float(v), 2) for k, v in zip(("ready", "data", "depart", "total"), acc)}
 
 
-def nccl_compare(lens, x, world: int, steps: int):
+def nccl_compare(lens, x, world: int, steps: int, flush=None):
     """NCCL comparison (tools/nccl_compare.py): ncclAllReduce(avg) per ring,
     issued back to back and coalesced into one NCCL group; the faster one is
-    the headline comparison."""
+    the headline comparison.  Same L2 policy as our timed steps."""
     from tools.nccl_compare import NcclRings
 
-    return NcclRings(x, lens).report(steps)
+    return NcclRings(x, lens).report(steps, flush)
 
 
 def main():
@@ -654,6 +692,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="bert")
     ap.add_argument("--acc", choices=["f64", "native"], default="f64")
     ap.add_argument("--lanes", type=int, default=1)
+    ap.add_argument("--l2-flush", choices=["auto", "on", "off"], default="auto",
+                    help="flush L2 between timed steps (auto: when the per-GPU inputs are < 2x L2)")
     ap.add_argument("--max-blocks", type=int, default=0, help="cap resident blocks of the cycle (0 = all SMs)")
     ap.add_argument("--protocol", choices=["auto", "pull", "push"], default="auto")
     ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")

@@ -9,6 +9,16 @@
 
 using KernelFn = void (*)(CycleParams);
 
+// RAVNEST_B200_MIN_CB (tests only): instantiate at least this member-count
+// bucket, so the CB = 8 / 16 kernels of 8- and 16-GPU jobs run, with fewer
+// members, on the GPUs a test box has.  Results are unchanged: every kernel
+// loops over the runtime C and uses CB only as a register-array bound.
+int bucket_c(int c) {
+  const char *e = getenv("RAVNEST_B200_MIN_CB");
+  const int floor = e ? atoi(e) : 0;
+  return floor > c ? std::min(floor, RV_MAX_CLUSTERS) : c;
+}
+
 enum Mode { kF32Acc64 = 0, kF32Native = 1, kF64 = 2 };
 
 // Vectors per thread per pass: U*C 16-byte loads in flight, kept within the
@@ -67,6 +77,7 @@ KernelFn pick_tma(int c, int *tv_out) {
 }
 
 KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
+  c = bucket_c(c);
   // RAVNEST_B200_TMA_VARIANT (experiments): 1 = 6 stages, 2 = 4 stages (one
   // block per SM), 3 = 8 stages of 16 KB, 4 = L2 evict-first hints
   const char *ve = getenv("RAVNEST_B200_TMA_VARIANT");
@@ -93,6 +104,7 @@ KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
 }
 
 KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
+  c = bucket_c(c);
   const char *ve = getenv("RAVNEST_B200_VARIANT");
   const int variant = ve ? atoi(ve) : 0;
   if (variant > 0 && mode == kF32Acc64 && vec && !push) {
@@ -118,5 +130,6 @@ KernelFn pick_ll(int c) {
 }
 
 KernelFn pick_ll_kernel(int mode, int c) {
+  c = bucket_c(c);
   return mode == kF32Native ? pick_ll<float>(c) : pick_ll<double>(c);
 }

@@ -75,7 +75,9 @@ def main():
         lens[0] += world - 1
         cases.append(lens)
     cases.append([1, 0, 2, world + 1, 3 * world - 1])      # tiny and zero-length rings
-    cases.append([26201088, 27168768, 27170304, 28942080])  # BERT-base rings
+    quick = os.environ.get("RAVNEST_DIST_QUICK") == "1"  # kernel-bucket / world-size variants
+    if not quick:
+        cases.append([26201088, 27168768, 27170304, 28942080])  # BERT-base rings
     failures = 0
     for ci, lens in enumerate(cases):
         total = sum(lens)
@@ -158,7 +160,8 @@ def main():
                     failures += 1
             dist.barrier()
             g.close()
-    failures += stall_phase(rank, world, local)
+    if not quick:
+        failures += stall_phase(rank, world, local)
     t = torch.tensor([failures])
     dist.all_reduce(t)
     if rank == 0:

@@ -147,6 +147,37 @@ def test_misaligned_and_ragged(dtype, c):
     assert bits_equal(got, want)
 
 
+@pytest.mark.parametrize("min_cb", [8, 16])
+def test_wider_kernel_buckets_same_bits(min_cb, monkeypatch):
+    # the CB = 8 / 16 instantiations (8- and 16-cluster jobs) run with fewer
+    # members: RAVNEST_B200_MIN_CB forces the bucket at plan build time
+    monkeypatch.setenv("RAVNEST_B200_MIN_CB", str(min_cb))
+    for c in (2, 3, 5):
+        lens = [100003, 7, 4096 + 5, 3 * c + 1]
+        sched = make_sched(lens, c)
+        rng = np.random.Generator(np.random.Philox(key=500 + c))
+        for dtype, np_dt, acc in ((torch.float32, np.float32, "f64"), (torch.float32, np.float32, "native"),
+                                  (torch.float64, np.float64, "f64")):
+            rows = [rng.normal(0, 3, sched.total_params).astype(np_dt) for _ in range(c)]
+            want = np.stack(ring_oracle.ring_mean([r.start for r in sched.rings], lens, rows, acc=acc)).astype(np_dt)
+            for offsets in (None, [1] * c, [m % 3 for m in range(c)]):  # TMA, vector pull, scalar pull
+                g = LocalRingGroup([r.start for r in sched.rings], lens, sched.total_params, [0] * c, dtype, acc=acc)
+                bufs = [torch.full((sched.total_params + 8,), -1234.5, dtype=dtype, device="cuda") for _ in range(c)]
+                off = [0] * c if offsets is None else offsets
+                views = [b[o:o + sched.total_params] for b, o in zip(bufs, off)]
+                for v, r in zip(views, rows):
+                    v.copy_(torch.from_numpy(r))
+                g.bind_tensors(views)
+                g.run()
+                torch.cuda.synchronize()
+                g.check()
+                assert bits_equal(np.stack([v.cpu().numpy() for v in views]), want), (c, acc, offsets)
+                for b, o in zip(bufs, off):
+                    h = b.cpu().numpy()
+                    assert (h[:o] == -1234.5).all() and (h[o + sched.total_params:] == -1234.5).all()
+                g.close()
+
+
 @pytest.mark.parametrize("lanes", [2, 4, 7, 16, 64])
 def test_lanes_match_single_launch(lanes):
     # lanes <= R group whole rings, lanes > R cut rings into pieces

@@ -55,7 +55,9 @@ class NcclRings:
             for v in self.views:
                 dist.all_reduce(v, op=dist.ReduceOp.AVG)
 
-    def time(self, fn, steps: int) -> float:
+    def time(self, fn, steps: int, flush=None) -> float:
+        """Mean ms per call; with `flush` (bench.L2Flush), L2 is flushed
+        before every call, outside its events."""
         import torch
         import torch.distributed as dist
 
@@ -64,22 +66,33 @@ class NcclRings:
         torch.cuda.synchronize()
         dist.barrier()
         s = torch.cuda.current_stream()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        for _ in range(steps):
-            fn()
-        b.record(s)
-        torch.cuda.synchronize()
-        t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64)
+        if flush is None:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(steps):
+                fn()
+            b.record(s)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / steps
+        else:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for a, b in evs:
+                flush(s)
+                a.record(s)
+                fn()
+                b.record(s)
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+        t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0])
 
-    def report(self, steps: int) -> dict:
+    def report(self, steps: int, flush=None) -> dict:
         out = {"algo": os.environ.get("NCCL_ALGO", "default"),
-               "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default")}
+               "nvls": os.environ.get("NCCL_NVLS_ENABLE", "default"), "l2_flushed": flush is not None}
         for name, fn in (("sequential", self.sequential), ("coalesced", self.coalesced)):
-            ms = self.time(fn, steps)
+            ms = self.time(fn, steps, flush)
             out[name] = {"ms_per_step": round(ms, 4),
                          "bus_gbps_per_gpu": round(_busbw(sum(self.lens), self.world, ms * 1e-3), 3)}
         # headline comparison: the faster NCCL variant
