@@ -114,7 +114,7 @@ struct rv_plan {
     std::vector<int> rings;  // rings meeting the range
     int grid = 0;
     // push
-    int64_t stride = 0, unit_vecs = 0, scatter_umax = 0;
+    int64_t stride = 0, unit_vecs = 0, scatter_umax = 0, umax_all = 0, push_lag = 0;
     std::vector<int64_t> ounits;
     std::vector<int> oseg_base;
   };
@@ -409,10 +409,26 @@ int build_tables(rv_plan *p) {
       lane.oseg_base[p->C] = (int)segs.size();
       lane.unit_vecs = unit_vecs;
       lane.scatter_umax = 0;
-      for (int q = 0; q < p->C; ++q)
+      lane.umax_all = 0;
+      for (int q = 0; q < p->C; ++q) {
         if (q != p->rank) lane.scatter_umax = std::max(lane.scatter_umax, lane.ounits[q]);
+        lane.umax_all = std::max(lane.umax_all, lane.ounits[q]);
+      }
+      // fold items start after `lag` units' scatters: that many rounds of
+      // the resident grid (RAVNEST_B200_PUSH_LAG, in rounds; default: every
+      // scatter first).  Derived from the schedule and the device model
+      // only, so every rank uses the same work order.
+      lane.push_lag = lane.umax_all;
+      if (const char *le = getenv("RAVNEST_B200_PUSH_LAG")) {
+        const double rounds = atof(le);
+        const int64_t cap = (int64_t)p->sm_count * p->occ;
+        if (rounds > 0)
+          lane.push_lag = std::min<int64_t>(lane.umax_all,
+                                            std::max<int64_t>(1, (int64_t)(rounds * cap / (p->C - 1) + 0.999)));
+      }
+      lane.n_tiles = ll ? (int64_t)(p->C - 1) * lane.scatter_umax * 2 + lane.ounits[p->rank]
+                        : (int64_t)p->C * lane.umax_all;
       lane.nseg = (int)segs.size();
-      lane.n_tiles = (int64_t)(p->C - 1) * lane.scatter_umax * (ll ? 2 : 1) + lane.ounits[p->rank];
       int rc = upload(lane, segs, {});
       if (rc) return rc;
     }
@@ -481,6 +497,10 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
     cp.stride = lane.stride;
     cp.units_max = p->units_max;
     cp.scatter_umax = lane.scatter_umax;
+    cp.umax_all = lane.umax_all;
+    cp.push_lag = lane.push_lag;
+    const char *de = getenv("RAVNEST_B200_PUSH_DYN");  // 0: static stride (tuning)
+    cp.push_dyn = de ? atoi(de) != 0 : 1;
     cp.unit_vecs = lane.unit_vecs;
   }
   if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet

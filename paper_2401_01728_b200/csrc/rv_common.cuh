@@ -61,7 +61,7 @@ struct LaneState {
   unsigned long long epoch;     // cycles completed on this lane
   unsigned long long signaled;  // last epoch whose arrive flags were posted
   unsigned int done;            // blocks finished in the running cycle
-  unsigned int pad;
+  unsigned int grab;            // push: work items handed out beyond the first one per block
 };
 
 struct CycleParams {
@@ -80,6 +80,9 @@ struct CycleParams {
   int64_t stride;              // push: staging elements per writer slot
   int64_t units_max;           // push: unit-flag slots per (lane, writer)
   int64_t scatter_umax;        // push: max units over the other owners
+  int64_t umax_all;            // push: max units over every owner (same on every rank)
+  int64_t push_lag;            // push: units scattered before the first fold item (1..umax_all)
+  int push_dyn;                // push: blocks take work items from a counter (else stride by grid)
   int64_t unit_vecs;           // push: vectors per unit
   int64_t ounits[RV_MAX_CLUSTERS];
   int oseg_base[RV_MAX_CLUSTERS + 1];
@@ -159,6 +162,16 @@ __device__ __forceinline__ void trace_max(const CycleParams &p, int slot) {
   if (p.trace) atomicMax(p.trace + slot, globaltimer());
 }
 
+// Next work item of a block: the items go out in position order, each block
+// taking a new one when it finishes its last (the first item of block b is
+// b).  Uniform across the block.
+__device__ __forceinline__ int64_t grab_next(const CycleParams &p, long long *s_next) {
+  __syncthreads();
+  if (threadIdx.x == 0) *s_next = (long long)gridDim.x + (long long)atomicAdd(&p.state->grab, 1u);
+  __syncthreads();
+  return *s_next;
+}
+
 // Exit barrier: the last block of this launch tells every peer that all of
 // this device's stores (local and remote) are done, then waits for theirs,
 // so nobody resumes training on a buffer a peer is still writing.
@@ -174,6 +187,7 @@ __device__ void depart(const CycleParams &p, unsigned long long epoch) {
       if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
       trace_max(p, 3);
       p.state->done = 0u;
+      p.state->grab = 0u;
       *(volatile unsigned long long *)&p.state->epoch = epoch;
       __threadfence();
     }

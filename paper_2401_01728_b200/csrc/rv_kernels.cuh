@@ -109,15 +109,30 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
   __syncthreads();
   const unsigned long long epoch = s_epoch;
   const int C = p.C, me = p.me;
-  const int64_t n_scatter = (int64_t)(C - 1) * p.scatter_umax;
-  const int64_t n_work = n_scatter + p.ounits[me];
+  // Work order (identical on every rank): the scatter items of the first
+  // `lag` units, then one fold item per C - 1 further scatter items, then
+  // the remaining folds.  A fold item only waits on peers' scatter items at
+  // earlier positions, so a co-resident grid always drains.
+  const int64_t ua = p.umax_all, lag = p.push_lag;
+  const int64_t head = lag * (C - 1), n_mix = (ua - lag) * C;
+  const int64_t n_work = ua * C;
   const unsigned long long t0 = globaltimer();
 
-  for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+  __shared__ long long s_next;
+  for (int64_t w = blockIdx.x; w < n_work; w = p.push_dyn ? grab_next(p, &s_next) : w + gridDim.x) {
     if (!s_ok) break;
-    if (w < n_scatter) {
-      const int r = (int)(w % (C - 1));
-      const int64_t u = w / (C - 1);
+    int64_t sidx = -1, fidx = -1;  // scatter item (unit * (C-1) + peer) or fold unit
+    if (w < head) {
+      sidx = w;
+    } else if (w - head < n_mix) {
+      const int64_t f = (w - head) / C, j = (w - head) % C;
+      if (j == 0) fidx = f; else sidx = (f + lag) * (C - 1) + (j - 1);
+    } else {
+      fidx = (ua - lag) + (w - head - n_mix);
+    }
+    if (sidx >= 0) {
+      const int r = (int)(sidx % (C - 1));
+      const int64_t u = sidx / (C - 1);
       int q = me + 1 + r;
       if (q >= C) q -= C;
       if (u >= p.ounits[q]) continue;
@@ -153,7 +168,8 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
       if (threadIdx.x == 0)
         st_release_sys(p.pflags[q] + pflag_index(p.lane, C, me, p.units_max, u), epoch);
     } else {
-      const int64_t u = w - n_scatter;
+      const int64_t u = fidx;
+      if (u >= p.ounits[me]) continue;
       const Seg s = find_unit<T>(p.segs + p.oseg_base[me], p.oseg_base[me + 1] - p.oseg_base[me], u);
       if (threadIdx.x == 0) {
         for (int m = 0; m < C && s_ok; ++m) {
