@@ -61,11 +61,13 @@ KernelFn pick_variant(int v, int *u_out) {
   }
 }
 
-// Co-resident TMA kernel: 32 KB of member data per pipeline stage
-// (CB * TV * 16 bytes), 3 stages -> 104 KB of shared memory, two blocks per
-// SM (measured best of 3/4/6 stages: 0.918 of measured HBM on BERT C=8).
-constexpr int kTmaStages = 3;
-constexpr int kTmaStageBytes = 32 * 1024;
+// Co-resident TMA kernel: 64 KB of member data per pipeline stage
+// (CB * TV * 16 bytes), 2 stages -> 136-192 KB of shared memory, one block
+// per SM.  Measured on BERT / ResNet-50 C=8 against 3 x 32 KB with two
+// blocks per SM (0.895 / 0.878 of measured HBM): 0.905-0.933 / 0.919-0.922;
+// 2 x 32/40/48/80/96 KB and 3 x 64 KB were slower (RAVNEST_B200_TMA_VARIANT).
+constexpr int kTmaStages = 2;
+constexpr int kTmaStageBytes = 64 * 1024;
 
 template <typename T, typename Acc, int STAGES, int STAGE_BYTES>
 KernelFn pick_tma(int c, int *tv_out) {
@@ -79,19 +81,29 @@ KernelFn pick_tma(int c, int *tv_out) {
 KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
   c = bucket_c(c);
   // RAVNEST_B200_TMA_VARIANT (experiments): 1 = 6 stages, 2 = 4 stages (one
-  // block per SM), 3 = 8 stages of 16 KB, 4 = L2 evict-first hints
+  // block per SM), 3 = 8 stages of 16 KB, 4 = L2 evict-first hints,
+  // 5 = 3 x 64 KB (one block per SM), 6 = 3 x 32 KB (two blocks per SM;
+  // the first default), 7 = 2 x 48 KB,
+  // 8 = 2 x 96 KB, 9 = 2 x 80 KB, 10 = 2 x 32 KB, 11 = 2 x 40 KB
   const char *ve = getenv("RAVNEST_B200_TMA_VARIANT");
   const int v = ve ? atoi(ve) : 0;
   int stages = kTmaStages;
   KernelFn k;
   if (v > 0 && mode == kF32Acc64) {
-    if (v == 1) { stages = 6; k = pick_tma<float, double, 6, kTmaStageBytes>(c, tv_out); }
-    else if (v == 2) { stages = 4; k = pick_tma<float, double, 4, kTmaStageBytes>(c, tv_out); }
+    if (v == 1) { stages = 6; k = pick_tma<float, double, 6, 32 * 1024>(c, tv_out); }
+    else if (v == 2) { stages = 4; k = pick_tma<float, double, 4, 32 * 1024>(c, tv_out); }
     else if (v == 4) {
       k = c <= 8 ? (KernelFn)ring_tma_kernel<float, double, 8, kTmaStageBytes / (8 * 16), kTmaStages, true>
                  : pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out);
       *tv_out = c <= 8 ? kTmaStageBytes / (8 * 16) : *tv_out;
     }
+    else if (v == 5) { stages = 3; k = pick_tma<float, double, 3, 64 * 1024>(c, tv_out); }
+    else if (v == 6) { stages = 3; k = pick_tma<float, double, 3, 32 * 1024>(c, tv_out); }
+    else if (v == 7) { stages = 2; k = pick_tma<float, double, 2, 48 * 1024>(c, tv_out); }
+    else if (v == 8) { stages = 2; k = pick_tma<float, double, 2, 96 * 1024>(c, tv_out); }
+    else if (v == 9) { stages = 2; k = pick_tma<float, double, 2, 80 * 1024>(c, tv_out); }
+    else if (v == 10) { stages = 2; k = pick_tma<float, double, 2, 32 * 1024>(c, tv_out); }
+    else if (v == 11) { stages = 2; k = pick_tma<float, double, 2, 40 * 1024>(c, tv_out); }
     else { stages = 8; k = pick_tma<float, double, 8, 16 * 1024>(c, tv_out); }
   } else {
     k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out)
