@@ -125,6 +125,7 @@ struct rv_plan {
   int block_threads = kThreads;
   size_t smem_bytes = 0;
   int max_blocks = 0;  // 0 = whole device; else cap on resident blocks (SM budget)
+  int push_dyn = 1;    // push: work items from a counter (RAVNEST_B200_PUSH_DYN=0: static stride)
 };
 
 namespace {
@@ -277,6 +278,10 @@ int build_tables(rv_plan *p) {
       if (!p->peer_push[r]) return set_err(RV_E_ARG, "push area of rank %d missing", r);
   }
   p->use_push = push;
+  {
+    const char *de = getenv("RAVNEST_B200_PUSH_DYN");  // tuning
+    p->push_dyn = de ? atoi(de) != 0 : 1;
+  }
   const bool ll = ll_active(p);
   if (ll && p->dtype != RV_DTYPE_F32) return set_err(RV_E_CONFIG, "the LL transport carries fp32 parameters only");
   const int mode = p->dtype == RV_DTYPE_F64 ? kF64 : (p->acc == RV_ACC_NATIVE ? kF32Native : kF32Acc64);
@@ -499,8 +504,7 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
     cp.scatter_umax = lane.scatter_umax;
     cp.umax_all = lane.umax_all;
     cp.push_lag = lane.push_lag;
-    const char *de = getenv("RAVNEST_B200_PUSH_DYN");  // 0: static stride (tuning)
-    cp.push_dyn = de ? atoi(de) != 0 : 1;
+    cp.push_dyn = p->push_dyn;
     cp.unit_vecs = lane.unit_vecs;
   }
   if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet
