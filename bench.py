@@ -355,6 +355,20 @@ def l2_policy(mode: str, input_bytes: int, device):
                              f"per-step event intervals")
 
 
+def launches_per_step(args, grp, total: int) -> int:
+    """Our kernels per rank per step at N > 1: one cycle kernel per lane,
+    plus the blend when it is not fused into the push kernel (rv_blend: one
+    vector launch, one more for a tail that is not a whole 16-byte vector)."""
+    n = args.lanes
+    if args.blend:
+        per_blend = 1 + (1 if total % 4 else 0)
+        if not args.fused_blend:
+            n += per_blend
+        elif grp.protocol != "push":
+            n += args.lanes * per_blend
+    return n
+
+
 def time_steps(fn, stream, steps: int, flush=None):
     """Per-step CUDA events on `stream`: (start, after-averaging, end).  The
     first interval is the averaging launch(es) alone -- the roofline basis.
@@ -390,6 +404,9 @@ def run_single(args):
         means = [torch.empty_like(x) for x in xs]
     g = LocalRingGroup(ring_starts(lens), lens, total, [0] * c, torch.float32, acc=args.acc, lanes=args.lanes)
     g.bind_tensors(xs, means)
+    in_cycle_blend = bool(args.blend and args.fused_blend)
+    if in_cycle_blend:
+        g.bind_live(lives)  # fused into the co-resident TMA kernel
     stream = torch.cuda.current_stream()
     lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
 
@@ -404,7 +421,7 @@ def run_single(args):
             g.run({0: [stream]})
         if mid is not None:
             mid.record(stream)
-        if args.blend:
+        if args.blend and not in_cycle_blend:
             for m in range(c):
                 blend_(lives[m], xs[m], means[m], stream)
 
@@ -461,7 +478,8 @@ def run_single(args):
 
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    hbm_bytes = 2 * c * total * 4
+    # the fused blend also reads and writes every live vector
+    hbm_bytes = (4 if in_cycle_blend else 2) * c * total * 4
     achieved = hbm_bytes / (kernel_ms * 1e-3) / 1e9
     bw = busbw(total, c, ms * 1e-3)
 
@@ -481,12 +499,16 @@ def run_single(args):
         "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
         "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                    "placement": "co-resident on cuda:0", "lanes": args.lanes, "parallelism": "replicas only",
-                   "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
+                   "blend": (f"snapshot average + delayed-update blend, tau={args.tau}, "
+                             + ("fused into the cycle kernel" if in_cycle_blend else "separate launches"))
+                   if args.blend else None,
                    "l2": l2_text},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4),
                      "traffic": ncu_traffic(args.workload, c, 1, args.acc) if not args.blend else None,
-                     "basis": f"2*C*S = {hbm_bytes} B per launch (read C, write C vectors)",
+                     "basis": (f"4*C*S = {hbm_bytes} B per launch (read C snapshots and C live vectors, "
+                               f"write C means and C live vectors)" if in_cycle_blend else
+                               f"2*C*S = {hbm_bytes} B per launch (read C, write C vectors)"),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
         "cpu_baseline": cpu_port,
         "cpu_threaded": cpu_threaded,
@@ -494,7 +516,8 @@ def run_single(args):
                 "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": c * total * 4, "d2h_bytes_per_step": c * total * 4,
                 "path": f"rv_allreduce_mean_host (pinned host fp32, {args.e2e_lanes} pipelined lanes)"},
-        "gpu_launches": args.steps * (args.lanes + (c if args.blend else 0)),
+        "gpu_launches": args.steps * (args.lanes + (0 if in_cycle_blend or not args.blend
+                                                     else c * (1 + (1 if total % 4 else 0)))),
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
@@ -518,8 +541,11 @@ def run_multi(args, rank: int, world: int, local_rank: int):
         # pending updates of `live` onto it (live <- mean + (live - snap))
         live = stale_live(x, rank, args.tau)
         mean = torch.empty_like(x)
+    # the blend rides in the cycle (rv_plan_bind_live): fused into the push
+    # kernel, or launched per lane by the C ABI for the other transports
+    in_cycle_blend = bool(args.blend and args.fused_blend)
     grp = DistRingGroup(src=x, dst=mean, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes,
-                        protocol=args.protocol, max_blocks=args.max_blocks)
+                        protocol=args.protocol, max_blocks=args.max_blocks, live=live if in_cycle_blend else None)
     stream = torch.cuda.current_stream()
     lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
 
@@ -534,7 +560,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             grp.average([stream])
         if mid is not None:
             mid.record(stream)
-        if args.blend:
+        if args.blend and not in_cycle_blend:
             blend_(live, x, mean, stream)
 
     clocks = ClockSampler(local_rank) if rank == 0 else None
@@ -618,7 +644,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                        "placement": "one cluster per GPU", "lanes": args.lanes, "protocol": grp.protocol,
                        "max_blocks": args.max_blocks or None,
-                       "blend": f"snapshot average + delayed-update blend, tau={args.tau}" if args.blend else None,
+                       "blend": (f"snapshot average + delayed-update blend, tau={args.tau}, "
+                                 + ("in the cycle (push: fused per unit)" if in_cycle_blend else "separate launch")) if args.blend else None,
                        "parallelism": f"multi-ring all-reduce over {world} GPUs (NVLink P2P)",
                        "l2": l2_text},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
@@ -633,7 +660,7 @@ def run_multi(args, rank: int, world: int, local_rank: int):
                     "h2d_bytes_per_step": world * total * 4, "d2h_bytes_per_step": world * total * 4,
                     "path": f"rv_allreduce_mean_host (pinned host fp32, {args.e2e_lanes} pipelined lanes)",
                     "host_cpus_rank0": numa_cpus or None},
-            "gpu_launches": args.steps * (args.lanes + (1 if args.blend else 0)) * world,
+            "gpu_launches": args.steps * world * launches_per_step(args, grp, total),
             "clocks": clk,
         }
         if nccl:
@@ -702,6 +729,8 @@ def main():
     ap.add_argument("--nccl", type=int, default=1)
     ap.add_argument("--blend", type=int, default=0, help="config 4: snapshot average + delayed-update blend")
     ap.add_argument("--tau", type=int, default=4)
+    ap.add_argument("--fused-blend", type=int, default=1,
+                    help="blend inside the cycle (rv_plan_bind_live) instead of separate launches")
     ap.add_argument("--trace", type=int, default=1, help="N>1: add a device-side phase trace")
     ap.add_argument("--numa-bind", type=int, default=1, help="bind ranks to their GPU's NUMA-local CPUs for e2e")
     ap.add_argument("--e2e-lanes", type=int, default=0,

@@ -95,6 +95,16 @@ int rv_plan_create(rv_plan **out, int device, int n_clusters, int n_rings,
  * Replaces the per-cluster working arrays (multiring.py:276,309). */
 int rv_plan_bind(rv_plan *plan, int pos, const void *src, void *dst);
 
+/* Delayed-update blend as part of the cycle (the stale
+ * updates of pipeline.py:384-411 landing on the average): with live bound on
+ * every local position, each cycle also leaves live <- mean + (live - src)
+ * there (exactly mean where live == src bitwise), src being the snapshot that
+ * was averaged and dst the mean.  src, dst and live must be distinct.  The
+ * push transport blends inside its kernel, unit by unit as the means land
+ * (no depart barrier); the others blend each lane's range right after its
+ * kernel, on the lane's stream.  live = NULL unbinds. */
+int rv_plan_bind_live(rv_plan *plan, int pos, void *live);
+
 /* Positions hosted by this device: their chunks are folded here. */
 int rv_plan_set_local(rv_plan *plan, const int *positions, int n_positions);
 

@@ -45,6 +45,7 @@ SIGNATURES = {
     "rv_plan_create": (ctypes.c_int, [_c_void_pp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_i64_p, _c_i64_p,
                                       ctypes.c_int64, ctypes.c_int, ctypes.c_int]),
     "rv_plan_bind": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "rv_plan_bind_live": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "rv_plan_set_local": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
     "rv_plan_set_lanes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rv_lane_ranges": (ctypes.c_int, [ctypes.c_int, _c_i64_p, _c_i64_p, ctypes.c_int, _c_i64_p, _c_i64_p]),

@@ -28,6 +28,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/ravnest_b200.h"
@@ -80,6 +81,7 @@ struct rv_plan {
   std::vector<int64_t> rstart, rlen;
   std::vector<const void *> src;
   std::vector<void *> dst;
+  std::vector<void *> live;  // delayed-update blend targets (rv_plan_bind_live), NULL = none
   std::vector<char> bound;
   std::vector<int> local;
   int n_lanes = 1;
@@ -114,7 +116,7 @@ struct rv_plan {
     std::vector<int> rings;  // rings meeting the range
     int grid = 0;
     // push
-    int64_t stride = 0, unit_vecs = 0, scatter_umax = 0, umax_all = 0, push_lag = 0;
+    int64_t stride = 0, unit_vecs = 0, scatter_umax = 0, umax_all = 0, push_lag = 0, blend_lag = 0;
     std::vector<int64_t> ounits;
     std::vector<int> oseg_base;
   };
@@ -126,6 +128,9 @@ struct rv_plan {
   size_t smem_bytes = 0;
   int max_blocks = 0;  // 0 = whole device; else cap on resident blocks (SM budget)
   int push_dyn = 1;    // push: work items from a counter (RAVNEST_B200_PUSH_DYN=0: static stride)
+  bool blend = false;        // live bound on the local positions: every cycle ends with the blend
+  bool fused_blend = false;  // ... inside the push kernel (else blend launches after each lane)
+  int64_t mflag_off = 0;     // push: mean-delivered flags after the scatter flags (u64 index)
 };
 
 namespace {
@@ -258,10 +263,22 @@ int build_tables(rv_plan *p) {
   const uintptr_t a = (uintptr_t)p->src[0] % 16;
   bool vec = true;
   for (int i = 0; i < p->C; ++i) {
-    if ((uintptr_t)p->src[i] % es || (uintptr_t)p->dst[i] % es)
+    if ((uintptr_t)p->src[i] % es || (uintptr_t)p->dst[i] % es || (uintptr_t)p->live[i] % es)
       return set_err(RV_E_ARG, "buffer of position %d is not %d-byte aligned", i, es);
     if ((uintptr_t)p->src[i] % 16 != a || (uintptr_t)p->dst[i] % 16 != a) vec = false;
+    if (p->live[i] && (uintptr_t)p->live[i] % 16 != a) vec = false;
   }
+  // delayed-update blend: all local positions or none; the means need their
+  // own buffer (the blend reads the snapshot = src after the means landed)
+  int n_live = 0;
+  for (int pos : p->local) n_live += p->live[pos] != nullptr;
+  if (n_live != 0 && n_live != (int)p->local.size())
+    return set_err(RV_E_ARG, "live buffers bound on %d of %d local positions", n_live, (int)p->local.size());
+  p->blend = n_live > 0;
+  if (p->blend)
+    for (int pos : p->local)
+      if (p->dst[pos] == p->src[pos] || p->live[pos] == p->src[pos] || p->live[pos] == p->dst[pos])
+        return set_err(RV_E_ARG, "blend at position %d needs distinct snapshot, mean and live buffers", pos);
   const int N = vec ? 16 / es : 1;
   const int64_t a0 = vec ? (int64_t)(a / es) : 0;
   p->ptrs_dirty = false;
@@ -278,6 +295,7 @@ int build_tables(rv_plan *p) {
       if (!p->peer_push[r]) return set_err(RV_E_ARG, "push area of rank %d missing", r);
   }
   p->use_push = push;
+  p->fused_blend = p->blend && push && p->proto == RV_PROTO_PUSH;  // co-resident TMA: set below
   {
     const char *de = getenv("RAVNEST_B200_PUSH_DYN");  // tuning
     p->push_dyn = de ? atoi(de) != 0 : 1;
@@ -297,7 +315,8 @@ int build_tables(rv_plan *p) {
     tile_vecs = kLLUnit;
   } else if (tma) {
     int tv = 0;
-    p->kernel = pick_tma_kernel(mode, p->C, &tv, &p->smem_bytes);
+    p->fused_blend = p->blend;
+    p->kernel = pick_tma_kernel(mode, p->C, p->blend, &tv, &p->smem_bytes);
     p->block_threads = kTmaConsumers + 32;
     RV_CUDA(cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem_bytes));
     tile_vecs = tv;
@@ -431,8 +450,12 @@ int build_tables(rv_plan *p) {
           lane.push_lag = std::min<int64_t>(lane.umax_all,
                                             std::max<int64_t>(1, (int64_t)(rounds * cap / (p->C - 1) + 0.999)));
       }
+      // fused blend: a unit's blends trail its fold by about one resident
+      // grid of items (RAVNEST_B200_BLEND_LAG: groups of C items, tuning)
+      lane.blend_lag = ((int64_t)p->sm_count * p->occ + p->C - 1) / p->C;
+      if (const char *be = getenv("RAVNEST_B200_BLEND_LAG")) lane.blend_lag = std::max(0, atoi(be));
       lane.n_tiles = ll ? (int64_t)(p->C - 1) * lane.scatter_umax * 2 + lane.ounits[p->rank]
-                        : (int64_t)p->C * lane.umax_all;
+                        : (int64_t)(p->fused_blend ? 2 * p->C - 1 : p->C) * lane.umax_all;
       lane.nseg = (int)segs.size();
       int rc = upload(lane, segs, {});
       if (rc) return rc;
@@ -470,6 +493,7 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
   for (int i = 0; i < p->C; ++i) {
     cp.src[i] = p->src[i];
     cp.dst[i] = p->dst[i];
+    cp.live[i] = p->live[i];
   }
   for (int r = 0; r < p->n_ranks && r < RV_MAX_RANKS; ++r) cp.peer_flags[r] = p->peer_flags[r];
   cp.segs = lane.segs;
@@ -505,6 +529,9 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
     cp.umax_all = lane.umax_all;
     cp.push_lag = lane.push_lag;
     cp.push_dyn = p->push_dyn;
+    cp.live_me = p->fused_blend ? p->live[p->rank] : nullptr;
+    cp.mflag_off = p->mflag_off;
+    cp.blend_lag = lane.blend_lag;
     cp.unit_vecs = lane.unit_vecs;
   }
   if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet
@@ -570,6 +597,7 @@ int rv_plan_create(rv_plan **out, int device, int n_clusters, int n_rings, const
   p->rlen.assign(ring_len, ring_len + n_rings);
   p->src.assign(n_clusters, nullptr);
   p->dst.assign(n_clusters, nullptr);
+  p->live.assign(n_clusters, nullptr);
   p->bound.assign(n_clusters, 0);
   p->peer_flags.assign(RV_MAX_RANKS, nullptr);
   if (const char *t = getenv("RAVNEST_B200_TIMEOUT_S")) {
@@ -605,6 +633,15 @@ int rv_plan_bind(rv_plan *p, int pos, const void *src, void *dst) {
   p->dst[pos] = dst;
   p->bound[pos] = 1;
   p->ptrs_dirty = true;
+  return RV_OK;
+}
+
+int rv_plan_bind_live(rv_plan *p, int pos, void *live) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  if (pos < 0 || pos >= p->C) return set_err(RV_E_ARG, "position %d out of range", pos);
+  p->live[pos] = live;
+  p->ptrs_dirty = true;
+  p->dirty = true;
   return RV_OK;
 }
 
@@ -676,8 +713,10 @@ int rv_plan_push_area(rv_plan *p, void **area, size_t *bytes) {
       p->pflag_bytes = 0;
       p->push_bytes = 2 * (size_t)p->C * p->stride_bound * 8;
     } else {
+      // [scatter flags | mean-delivered flags (fused blend)], one per (lane, peer, unit) each
       const size_t nflags = (size_t)std::max(1, p->n_lanes) * p->C * p->units_max;
-      p->pflag_bytes = (nflags * sizeof(unsigned long long) + 4095) / 4096 * 4096;
+      p->mflag_off = (int64_t)nflags;
+      p->pflag_bytes = (2 * nflags * sizeof(unsigned long long) + 4095) / 4096 * 4096;
       p->push_bytes = p->pflag_bytes + (size_t)p->C * p->stride_bound * elem_size(p->dtype);
     }
     DeviceGuard g(p->device);
@@ -764,10 +803,22 @@ int rv_allreduce_mean(rv_plan *p, void *const *streams, int n_streams) {
     int rc = build_tables(p);
     if (rc) return rc;
   }
+  const int es = elem_size(p->dtype);
   for (int l = 0; l < p->n_lanes; ++l) {
     cudaStream_t st = (streams && n_streams > 0) ? (cudaStream_t)streams[l % n_streams] : (cudaStream_t)0;
     int rc = launch_lane(p, l, st);
     if (rc) return rc;
+    if (p->blend && !p->fused_blend) {
+      // transports without the fused blend: the lane's means are final when
+      // its kernel ends, so the blend of the lane's range follows on its stream
+      const rv_plan::Lane &lane = p->lanes[l];
+      const size_t off = (size_t)lane.lo * es;
+      for (int pos : p->local) {
+        rc = rv_blend(p->device, p->dtype, (char *)p->live[pos] + off, (const char *)p->src[pos] + off,
+                      (const char *)p->dst[pos] + off, lane.hi - lane.lo, st);
+        if (rc) return rc;
+      }
+    }
   }
   return RV_OK;
 }
@@ -780,6 +831,7 @@ int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const 
     int rc = build_tables(p);
     if (rc) return rc;
   }
+  if (p->blend) return set_err(RV_E_ARG, "the host-buffer path does not blend (unbind the live buffers)");
   const int es = elem_size(p->dtype);
   // host->device copies run lane after lane (lane l's kernel starts as soon
   // as its own inputs have landed, while lane l+1's copy streams in and lane

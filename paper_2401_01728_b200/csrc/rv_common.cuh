@@ -83,6 +83,10 @@ struct CycleParams {
   int64_t umax_all;            // push: max units over every owner (same on every rank)
   int64_t push_lag;            // push: units scattered before the first fold item (1..umax_all)
   int push_dyn;                // push: blocks take work items from a counter (else stride by grid)
+  void *live[RV_MAX_CLUSTERS]; // co-resident (TMA), fused blend: every member's live buffer
+  void *live_me;               // push, fused blend: this rank's live buffer (else NULL)
+  int64_t mflag_off;           // push, fused blend: mean-delivered flags, offset in a push area's flags
+  int64_t blend_lag;           // push, fused blend: groups between a fold item and the blends of its unit
   int64_t unit_vecs;           // push: vectors per unit
   int64_t ounits[RV_MAX_CLUSTERS];
   int oseg_base[RV_MAX_CLUSTERS + 1];
@@ -175,7 +179,9 @@ __device__ __forceinline__ int64_t grab_next(const CycleParams &p, long long *s_
 // Exit barrier: the last block of this launch tells every peer that all of
 // this device's stores (local and remote) are done, then waits for theirs,
 // so nobody resumes training on a buffer a peer is still writing.
-__device__ void depart(const CycleParams &p, unsigned long long epoch) {
+// With `cross` false (push with the fused blend, where every write into this
+// rank's buffers is awaited item by item) only the lane bookkeeping remains.
+__device__ void depart(const CycleParams &p, unsigned long long epoch, bool cross = true) {
   __syncthreads();
   if (threadIdx.x == 0) {
     trace_max(p, 2);
@@ -183,8 +189,10 @@ __device__ void depart(const CycleParams &p, unsigned long long epoch) {
     const unsigned prev = atomicAdd(&p.state->done, 1u);
     if (prev == gridDim.x - 1) {
       __threadfence_system();
-      post_peers(p, 1, epoch);
-      if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
+      if (cross) {
+        post_peers(p, 1, epoch);
+        if (*(volatile unsigned *)p.status == 0) wait_peers(p, 1, epoch);
+      }
       trace_max(p, 3);
       p.state->done = 0u;
       p.state->grab = 0u;

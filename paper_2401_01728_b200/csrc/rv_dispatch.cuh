@@ -69,17 +69,37 @@ KernelFn pick_variant(int v, int *u_out) {
 constexpr int kTmaStages = 2;
 constexpr int kTmaStageBytes = 64 * 1024;
 
-template <typename T, typename Acc, int STAGES, int STAGE_BYTES>
+// BL: the fused-blend kernel; a stage carries C src and C live tiles, so the
+// same stage bytes hold half the vectors per member.
+template <typename T, typename Acc, int STAGES, int STAGE_BYTES, bool BL = false>
 KernelFn pick_tma(int c, int *tv_out) {
-  if (c <= 2) { *tv_out = STAGE_BYTES / (2 * 16); return ring_tma_kernel<T, Acc, 2, STAGE_BYTES / (2 * 16), STAGES>; }
-  if (c <= 4) { *tv_out = STAGE_BYTES / (4 * 16); return ring_tma_kernel<T, Acc, 4, STAGE_BYTES / (4 * 16), STAGES>; }
-  if (c <= 8) { *tv_out = STAGE_BYTES / (8 * 16); return ring_tma_kernel<T, Acc, 8, STAGE_BYTES / (8 * 16), STAGES>; }
-  *tv_out = STAGE_BYTES / (16 * 16);
-  return ring_tma_kernel<T, Acc, 16, STAGE_BYTES / (16 * 16), STAGES>;
+  constexpr int K = BL ? 2 : 1;
+  if (c <= 2) {
+    *tv_out = STAGE_BYTES / (K * 2 * 16);
+    return ring_tma_kernel<T, Acc, 2, STAGE_BYTES / (K * 2 * 16), STAGES, false, BL>;
+  }
+  if (c <= 4) {
+    *tv_out = STAGE_BYTES / (K * 4 * 16);
+    return ring_tma_kernel<T, Acc, 4, STAGE_BYTES / (K * 4 * 16), STAGES, false, BL>;
+  }
+  if (c <= 8) {
+    *tv_out = STAGE_BYTES / (K * 8 * 16);
+    return ring_tma_kernel<T, Acc, 8, STAGE_BYTES / (K * 8 * 16), STAGES, false, BL>;
+  }
+  *tv_out = STAGE_BYTES / (K * 16 * 16);
+  return ring_tma_kernel<T, Acc, 16, STAGE_BYTES / (K * 16 * 16), STAGES, false, BL>;
 }
 
-KernelFn pick_tma_kernel(int mode, int c, int *tv_out, size_t *smem_out) {
+KernelFn pick_tma_kernel(int mode, int c, bool blend, int *tv_out, size_t *smem_out) {
   c = bucket_c(c);
+  if (blend) {
+    KernelFn k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes, true>(c, tv_out)
+               : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes, true>(c, tv_out)
+                                    : pick_tma<double, double, kTmaStages, kTmaStageBytes, true>(c, tv_out);
+    const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
+    *smem_out = (size_t)kTmaStages * 2 * cb * (*tv_out) * 16 + 2 * (size_t)(cb + 1) * (*tv_out) * 16;
+    return k;
+  }
   // RAVNEST_B200_TMA_VARIANT (experiments): 1 = 6 stages, 2 = 4 stages (one
   // block per SM), 3 = 8 stages of 16 KB, 4 = L2 evict-first hints,
   // 5 = 3 x 64 KB (one block per SM), 6 = 3 x 32 KB (two blocks per SM;

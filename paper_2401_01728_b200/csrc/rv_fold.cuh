@@ -42,17 +42,36 @@ __device__ __forceinline__ const T *member_elem(const CycleParams &p, const Seg 
   return static_cast<const T *>(p.stage[p.me]) + ((int64_t)m * p.stride + s.stage_off + (i - s.lo));
 }
 
+// Delayed-update blend of one value, live <- mean + (live - snap), two
+// roundings in the storage type; where live and snap are the same bits the
+// result is mean itself (oracle/ring_oracle.blend, blend_kernel).
+template <typename T>
+__device__ __forceinline__ T blend_one(T mean, T live, T snap) {
+  using U = typename std::conditional<sizeof(T) == 8, unsigned long long, unsigned>::type;
+  U lb, sb;
+  memcpy(&lb, &live, sizeof(T));
+  memcpy(&sb, &snap, sizeof(T));
+  return lb == sb ? mean : mean + (live - snap);
+}
+
 // Fold of one element (chunk edges, misaligned buffers): ring order from s.k.
+// Push with the fused blend: the owner (s.k == me) also blends its own live
+// value, its snapshot being the first member folded.
 template <typename T, typename Acc, bool PUSH>
 __device__ __forceinline__ void fold_scalar(const CycleParams &p, const Seg &s, int64_t i) {
   int m = s.k;
-  Acc acc = (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
+  const T first = __ldcs(member_elem<T, PUSH>(p, s, m, i));
+  Acc acc = (Acc)first;
   for (int q = 1; q < p.C; ++q) {
     m = (m + 1 == p.C) ? 0 : m + 1;
     acc = acc + (Acc)__ldcs(member_elem<T, PUSH>(p, s, m, i));
   }
   const T out = finish<T, Acc>(acc, p);
   for (int q = 0; q < p.C; ++q) __stcs(static_cast<T *>(p.dst[q]) + i, out);
+  if (PUSH && p.live_me) {
+    T *live = static_cast<T *>(p.live_me) + i;
+    *live = blend_one<T>(out, *live, first);
+  }
 }
 
 // Fold one pass of chunk s: this thread takes vectors j0 + u*kThreads
@@ -95,6 +114,14 @@ __device__ __forceinline__ void fold_pass(const CycleParams &p, const Seg &s, in
 #pragma unroll
       for (int q = 0; q < CB; ++q)
         if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
+      if (PUSH && p.live_me) {  // fused blend of the owner's own copy (x[u][0] is its snapshot)
+        Raw *lp = reinterpret_cast<Raw *>(static_cast<T *>(p.live_me) + i);
+        Lanes<T, VB> l;
+        l.raw = *lp;
+#pragma unroll
+        for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(out.v[e], l.v[e], x[u][0].v[e]);
+        *lp = l.raw;
+      }
     }
   }
 }

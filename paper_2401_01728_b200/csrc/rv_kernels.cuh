@@ -113,17 +113,67 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
   // `lag` units, then one fold item per C - 1 further scatter items, then
   // the remaining folds.  A fold item only waits on peers' scatter items at
   // earlier positions, so a co-resident grid always drains.
-  const int64_t ua = p.umax_all, lag = p.push_lag;
+  // With the fused blend: every scatter item, then groups of C items, group
+  // g = fold unit g, then the blend items of unit g - blend_lag of the C - 1
+  // other owners (each waits for that owner's mean-delivered flag, set by a
+  // fold item blend_lag groups earlier), so the blend's HBM traffic runs
+  // under the NVLink traffic of later folds and finds the means in L2.
+  const int64_t ua = p.umax_all;
+  const bool fused = p.live_me != nullptr;
+  const int64_t lag = fused ? ua : p.push_lag, blag = p.blend_lag;
   const int64_t head = lag * (C - 1), n_mix = (ua - lag) * C;
-  const int64_t n_work = ua * C;
+  const int64_t n_work = fused ? head + (ua + blag) * C : ua * C;
   const unsigned long long t0 = globaltimer();
 
   __shared__ long long s_next;
   for (int64_t w = blockIdx.x; w < n_work; w = p.push_dyn ? grab_next(p, &s_next) : w + gridDim.x) {
     if (!s_ok) break;
     int64_t sidx = -1, fidx = -1;  // scatter item (unit * (C-1) + peer) or fold unit
+    if (fused && w >= head && (w - head) % C != 0) {
+      // blend item: unit u of owner q, from q's means in this rank's dst
+      const int r = (int)((w - head) % C) - 1;
+      const int64_t u = (w - head) / C - blag;
+      int q = me + 1 + r;
+      if (q >= C) q -= C;
+      if (u < 0 || u >= p.ounits[q]) continue;
+      const Seg s = find_unit<T>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
+      if (threadIdx.x == 0) {
+        const unsigned diag = (3u << 16) | ((unsigned)p.lane << 8) | (unsigned)q;
+        if (!wait_flag(p, p.pflags[me] + p.mflag_off + pflag_index(p.lane, C, q, p.units_max, u), epoch, t0, diag))
+          s_ok = 0;
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      const int64_t uu = u - s.unit0;
+      const int64_t nvec = (s.body_hi - s.body_lo) / N;
+      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
+      const T *mean = static_cast<const T *>(p.dst[me]);
+      const T *snap = static_cast<const T *>(p.src[me]);
+      T *live = static_cast<T *>(p.live_me);
+      for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
+        const int64_t i = s.body_lo + j * N;
+        Lanes<T, VB> m, l, sn;
+        m.raw = __ldcg(reinterpret_cast<const Raw *>(mean + i));
+        sn.raw = __ldcs(reinterpret_cast<const Raw *>(snap + i));
+        l.raw = *reinterpret_cast<const Raw *>(live + i);
+#pragma unroll
+        for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(m.v[e], l.v[e], sn.v[e]);
+        *reinterpret_cast<Raw *>(live + i) = l.raw;
+      }
+      if (uu == 0) {
+        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+        if ((int64_t)threadIdx.x < nhead + ntail) {
+          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
+                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
+          live[i] = blend_one<T>(__ldcg(mean + i), live[i], snap[i]);
+        }
+      }
+      continue;
+    }
     if (w < head) {
       sidx = w;
+    } else if (fused) {
+      fidx = (w - head) / C;  // j == 0 of group g
     } else if (w - head < n_mix) {
       const int64_t f = (w - head) / C, j = (w - head) % C;
       if (j == 0) fidx = f; else sidx = (f + lag) * (C - 1) + (j - 1);
@@ -193,10 +243,18 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
           fold_scalar<T, Acc, true>(p, s, i);
         }
       }
+      if (fused) {
+        // the means of this unit are in every member's dst: tell them
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0)
+          for (int m = 0; m < C; ++m)
+            if (m != me) st_release_sys(p.pflags[m] + p.mflag_off + pflag_index(p.lane, C, me, p.units_max, u), epoch);
+      }
       __syncthreads();  // s_ok is re-armed by thread 0 for the next unit
     }
   }
-  depart(p, epoch);
+  depart(p, epoch, !fused);
 }
 
 // ---------------------------------------------------------------------------
@@ -427,13 +485,18 @@ __device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigne
                : "memory");
 }
 
-template <typename T, typename Acc, int CB, int TV, int STAGES, bool HINT = false>
+// BL (fused delayed-update blend): each stage also carries every member's
+// live tile; the consumers write the mean tile and C blended live tiles,
+// which go out by bulk store to dst and live.
+template <typename T, typename Acc, int CB, int TV, int STAGES, bool HINT = false, bool BL = false>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 2)
 ring_tma_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = 16 / sizeof(T);
+  constexpr int SLOTS = BL ? 2 * CB : CB;  // tiles per stage: src (ring order), then live
+  constexpr int OUTS = BL ? CB + 1 : 1;    // output tiles: mean, then blended live
   extern __shared__ __align__(128) unsigned char smem[];
-  uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][CB][TV]
-  uint4 *out = in + (size_t)STAGES * CB * TV;                          // [2][TV]
+  uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][SLOTS][TV]
+  uint4 *out = in + (size_t)STAGES * SLOTS * TV;                       // [2][OUTS][TV]
   __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
   const int tid = threadIdx.x;
   const int C = p.C;
@@ -471,17 +534,21 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
         const int64_t j0 = lt * TV;
         const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
         if (n >= STAGES) mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], (unsigned)(cnt * 16 * C));
+        mbar_expect_tx(&full[stage], (unsigned)(cnt * 16 * C * (BL ? 2 : 1)));
         if (cnt > 0) {
           for (int q = 0; q < C; ++q) {
             int m = s.k + q;
             if (m >= C) m -= C;
             if constexpr (HINT)
-              bulk_load_hint(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
-                             (unsigned)(cnt * 16), &full[stage], evict_first_policy());
+              bulk_load_hint(in + ((size_t)stage * SLOTS + q) * TV,
+                             static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N, (unsigned)(cnt * 16),
+                             &full[stage], evict_first_policy());
             else
-              bulk_load(in + ((size_t)stage * CB + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
+              bulk_load(in + ((size_t)stage * SLOTS + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
                         (unsigned)(cnt * 16), &full[stage]);
+            if constexpr (BL)
+              bulk_load(in + ((size_t)stage * SLOTS + CB + q) * TV,
+                        static_cast<const T *>(p.live[m]) + s.body_lo + j0 * N, (unsigned)(cnt * 16), &full[stage]);
           }
         }
         if (++stage == STAGES) {
@@ -510,32 +577,53 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
     for (int v = c; v < cnt; v += kTmaConsumers) {
       Lanes<T, 16> x, o;
       Acc acc[N];
-      x.raw = in[((size_t)stage * CB + 0) * TV + v];
+      x.raw = in[((size_t)stage * SLOTS + 0) * TV + v];
 #pragma unroll
       for (int e = 0; e < N; ++e) acc[e] = (Acc)x.v[e];
 #pragma unroll
       for (int q = 1; q < CB; ++q) {
         if (q < C) {
-          x.raw = in[((size_t)stage * CB + q) * TV + v];
+          x.raw = in[((size_t)stage * SLOTS + q) * TV + v];
 #pragma unroll
           for (int e = 0; e < N; ++e) acc[e] = acc[e] + (Acc)x.v[e];
         }
       }
 #pragma unroll
       for (int e = 0; e < N; ++e) o.v[e] = finish<T, Acc>(acc[e], p);
-      out[ob * TV + v] = o.raw;
+      out[(size_t)ob * OUTS * TV + v] = o.raw;
+      if constexpr (BL) {
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          if (q < C) {
+            Lanes<T, 16> sn, l;
+            sn.raw = in[((size_t)stage * SLOTS + q) * TV + v];
+            l.raw = in[((size_t)stage * SLOTS + CB + q) * TV + v];
+#pragma unroll
+            for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(o.v[e], l.v[e], sn.v[e]);
+            out[((size_t)ob * OUTS + 1 + q) * TV + v] = l.raw;
+          }
+        }
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
     if (c == 0) {
       mbar_arrive(&empty[stage]);  // every consumer has read this stage
       if (cnt > 0) {
+        const uint4 *mean_tile = out + (size_t)ob * OUTS * TV;
         for (int q = 0; q < C; ++q)
           if constexpr (HINT)
-            bulk_store_hint(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16),
+            bulk_store_hint(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, mean_tile, (unsigned)(cnt * 16),
                             evict_first_policy());
           else
-            bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, out + ob * TV, (unsigned)(cnt * 16));
+            bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, mean_tile, (unsigned)(cnt * 16));
+        if constexpr (BL)
+          for (int q = 0; q < C; ++q) {
+            int m = s.k + q;
+            if (m >= C) m -= C;
+            bulk_store(static_cast<T *>(p.live[m]) + s.body_lo + j0 * N, mean_tile + (size_t)(1 + q) * TV,
+                       (unsigned)(cnt * 16));
+          }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // out[ob ^ 1] reusable
@@ -545,6 +633,11 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
       if ((int64_t)c < nhead + ntail) {
         const int64_t i = (int64_t)c < nhead ? s.lo + c : s.body_hi + ((int64_t)c - nhead);
         fold_scalar<T, Acc, false>(p, s, i);
+        if constexpr (BL)
+          for (int m = 0; m < C; ++m) {
+            T *l = static_cast<T *>(p.live[m]) + i;
+            *l = blend_one<T>(static_cast<const T *>(p.dst[m])[i], *l, static_cast<const T *>(p.src[m])[i]);
+          }
       }
     }
     ob ^= 1;

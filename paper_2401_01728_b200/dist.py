@@ -82,7 +82,9 @@ class DistRingGroup:
     """Collective multi-ring averaging of one CUDA buffer per rank.
 
     ``src`` is read and ``dst`` (default: ``src``, i.e. in place) written;
-    both must stay allocated while the group lives.  All ranks must call
+    both must stay allocated while the group lives.  With ``live`` (and a
+    separate ``dst``), every cycle also applies the delayed-update blend
+    live <- mean + (live - src) (``bind_live``).  All ranks must call
     ``average`` the same number of times in the same order, as with any
     collective.
     """
@@ -90,7 +92,7 @@ class DistRingGroup:
     def __init__(self, schedule=None, src=None, dst=None, *, starts: Sequence[int] | None = None,
                  lens: Sequence[int] | None = None, cluster_id: int | None = None, acc: str = "f64",
                  lanes: int = 1, group=None, timeout_s: float | None = None, protocol: str = "auto",
-                 max_blocks: int = 0):
+                 max_blocks: int = 0, live=None):
         import torch.distributed as dist
 
         if src is None:
@@ -171,7 +173,26 @@ class DistRingGroup:
         self.plan.set_peers(self.position, self.world, areas)
         if protocol in ("push", "ll"):
             self.plan.set_push_peers(push_areas)
+        self.live = None
+        if live is not None:
+            self.bind_live(live)
         dist.barrier(group=group)
+
+    def bind_live(self, live) -> None:
+        """Fuse the delayed-update blend into every cycle: ``live`` (this
+        rank's live parameters) ends each cycle as mean + (live - src), the
+        snapshot ``src`` having been averaged into ``dst``.  ``None`` unbinds.
+        Local to this rank; every rank should bind or none (the push kernel
+        then blends unit by unit as the means land)."""
+        if live is not None:
+            if not live.is_cuda or not live.is_contiguous() or live.numel() != self.total:
+                raise LayoutError("live must be a contiguous CUDA tensor shaped like the parameter vector")
+            if live.dtype != self.src.dtype or live.device.index != self.device:
+                raise LayoutError("live must match the parameter buffer's dtype and device")
+            if self.dst.data_ptr() == self.src.data_ptr():
+                raise LayoutError("the fused blend needs a separate mean buffer (dst) besides the snapshot (src)")
+        self.plan.bind_live(self.position, None if live is None else live.data_ptr())
+        self.live = live
 
     def average(self, streams=None) -> None:
         """Launch one cycle on ``streams`` (default: the current stream)."""

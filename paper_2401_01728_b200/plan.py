@@ -68,6 +68,12 @@ class DevicePlan:
         N.check(self.lib.rv_plan_bind(self._h, int(pos), ctypes.c_void_p(int(src_ptr)),
                                       ctypes.c_void_p(int(dst_ptr))), "rv_plan_bind")
 
+    def bind_live(self, pos: int, live_ptr: int | None) -> None:
+        """Blend target of position ``pos`` (``None`` unbinds): every cycle
+        then also leaves live <- mean + (live - src) there."""
+        N.check(self.lib.rv_plan_bind_live(self._h, int(pos), ctypes.c_void_p(int(live_ptr or 0))),
+                "rv_plan_bind_live")
+
     def set_local(self, positions: Iterable[int]) -> None:
         pos = [int(p) for p in positions]
         arr = (ctypes.c_int * max(1, len(pos)))(*pos)
@@ -224,6 +230,21 @@ class LocalRingGroup:
             if not (s.is_contiguous() and d.is_contiguous()):
                 raise LayoutError(f"cluster position {m} tensor must be contiguous")
             self.bind(m, s.data_ptr(), d.data_ptr())
+
+    def bind_live(self, lives: Sequence | None) -> None:
+        """Delayed-update blend fused into the cycle: ``lives[m]`` (a tensor
+        like position m's src) ends every cycle as mean + (live - src).
+        Needs separate src and dst buffers.  ``None`` unbinds."""
+        for m in range(self.n_clusters):
+            ptr = None
+            if lives is not None:
+                t = lives[m]
+                if t.device.index != self.devices[m] or t.numel() != self.total or not t.is_contiguous():
+                    raise LayoutError(f"live tensor of position {m} does not match its cluster vector")
+                ptr = t.data_ptr()
+            for d, plan in self.plans.items():
+                if d == self.devices[m]:
+                    plan.bind_live(m, ptr)
 
     def run(self, streams: dict | None = None) -> None:
         """Launch one cycle.  ``streams`` maps device -> stream (or a list of

@@ -61,6 +61,57 @@ def stall_phase(rank, world, local):
     return failures
 
 
+def blend_phase(rank, world, local):
+    """Delayed-update blend inside the cycle (DistRingGroup(live=...)):
+    mean = ring mean of the snapshots, live <- mean + (live - snap), bitwise
+    against the oracle, over three back-to-back cycles without host syncs
+    (the fused push path has no depart barrier).  Guard bands on all three
+    buffers."""
+    failures = 0
+    lens = [200003, 5, 77777, 2 * world + 1]
+    total = sum(lens)
+    starts = list(np.cumsum([0] + lens[:-1]))
+    for proto in ("push", "pull", "ll"):
+        for dt, lanes in ((torch.float32, 1), (torch.float32, 3), (torch.float64, 1)):
+            if proto == "ll" and dt == torch.float64:
+                continue
+            npdt = np.float32 if dt == torch.float32 else np.float64
+            snaps = [np.random.Generator(np.random.Philox(key=500 + m)).normal(0, 1, total).astype(npdt)
+                     for m in range(world)]
+            lives = [s + np.random.Generator(np.random.Philox(key=600 + m)).normal(0, 1e-3, total).astype(npdt)
+                     for m, s in enumerate(snaps)]
+            for m in range(world):  # some entries untouched since the snapshot: exactly the mean there
+                lives[m][::7] = snaps[m][::7]
+            bufs = [torch.full((total + 16,), -1234.5, dtype=dt, device=f"cuda:{local}") for _ in range(3)]
+            x, mean, live = (b[8:8 + total] for b in bufs)
+            x.copy_(torch.from_numpy(snaps[rank]))
+            live.copy_(torch.from_numpy(lives[rank]))
+            g = DistRingGroup(src=x, dst=mean, starts=starts, lens=lens, lanes=lanes, protocol=proto, live=live)
+            streams = [torch.cuda.Stream() for _ in range(lanes)]
+            for st in streams:
+                st.wait_stream(torch.cuda.current_stream())
+            for _ in range(3):
+                g.average(streams)
+            torch.cuda.synchronize()
+            g.check()
+            want_mean = ring_oracle.ring_mean(starts, lens, snaps)[rank].astype(npdt)
+            want_live = lives[rank]
+            for _ in range(3):
+                want_live = ring_oracle.blend(want_mean, want_live, snaps[rank])
+            ok = np.array_equal(bits(mean.cpu().numpy()), bits(want_mean))
+            ok = ok and np.array_equal(bits(live.cpu().numpy()), bits(want_live))
+            ok = ok and np.array_equal(bits(x.cpu().numpy()), bits(snaps[rank]))  # snapshot untouched
+            for b in bufs:
+                h = b.cpu().numpy()
+                ok = ok and (h[:8] == -1234.5).all() and (h[8 + total:] == -1234.5).all()
+            if not ok:
+                print(f"rank {rank} blend {proto} {dt} lanes={lanes}: mismatch", flush=True)
+                failures += 1
+            dist.barrier()
+            g.close()
+    return failures
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -160,6 +211,7 @@ def main():
                     failures += 1
             dist.barrier()
             g.close()
+    failures += blend_phase(rank, world, local)
     if not quick:
         failures += stall_phase(rank, world, local)
     t = torch.tensor([failures])

@@ -291,6 +291,51 @@ def test_blend_matches_oracle():
         assert bits_equal(lt.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("lanes,offsets", [(1, (0, 0, 0)), (5, (0, 0, 0)), (1, (1, 1, 1)), (3, (0, 1, 2))])
+def test_blend_in_cycle_co_resident(lanes, offsets):
+    # rv_plan_bind_live on one GPU: fused into the TMA kernel (congruent
+    # buffers, offsets 0 / 1), or blended after each lane's register kernel
+    # (incongruent offsets); guard bands around every buffer
+    c = 3
+    lens = [100003, 9, 4096 + 3]
+    sched = make_sched(lens, c)
+    starts = [r.start for r in sched.rings]
+    rng = np.random.Generator(np.random.Philox(key=71))
+    snaps = [rng.normal(0, 1, sched.total_params).astype(np.float32) for _ in range(c)]
+    lives = [s + rng.normal(0, 1e-3, s.size).astype(np.float32) for s in snaps]
+    mean_want = np.stack(ring_oracle.ring_mean(starts, lens, snaps)).astype(np.float32)
+    live_want = [ring_oracle.blend(mean_want[m], lives[m], snaps[m]) for m in range(c)]
+    g = LocalRingGroup(starts, lens, sched.total_params, [0] * c, torch.float32, lanes=lanes)
+    n = sched.total_params
+    bufs = [[torch.full((n + 8,), -1234.5, device="cuda") for _ in range(3)] for _ in range(c)]
+    xs = [bufs[m][0][offsets[0]:offsets[0] + n] for m in range(c)]
+    means = [bufs[m][1][offsets[1]:offsets[1] + n] for m in range(c)]
+    lv = [bufs[m][2][offsets[2]:offsets[2] + n] for m in range(c)]
+    for m in range(c):
+        xs[m].copy_(torch.from_numpy(snaps[m]))
+        lv[m].copy_(torch.from_numpy(lives[m]))
+    g.bind_tensors(xs, means)
+    g.bind_live(lv)
+    streams = [torch.cuda.Stream() for _ in range(lanes)]
+    for st in streams:
+        st.wait_stream(torch.cuda.current_stream())
+    g.run({0: streams})
+    torch.cuda.synchronize()
+    g.check()
+    assert bits_equal(np.stack([t.cpu().numpy() for t in means]), mean_want)
+    assert bits_equal(np.stack([t.cpu().numpy() for t in lv]), np.stack(live_want))
+    assert bits_equal(np.stack([t.cpu().numpy() for t in xs]), np.stack(snaps))
+    for m in range(c):
+        for b, o in zip(bufs[m], offsets):
+            h = b.cpu().numpy()
+            assert (h[:o] == -1234.5).all() and (h[o + n:] == -1234.5).all()
+    # in place (dst == src) cannot blend: the snapshot would be gone
+    g.bind_tensors(xs)
+    with pytest.raises(rv.RavnestError):
+        g.run()
+    g.close()
+
+
 def test_errors_map_to_reference_classes():
     sched = make_sched([10], 2)
     with pytest.raises(rv.ConfigError):
