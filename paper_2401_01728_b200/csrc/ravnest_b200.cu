@@ -450,9 +450,11 @@ int build_tables(rv_plan *p) {
           lane.push_lag = std::min<int64_t>(lane.umax_all,
                                             std::max<int64_t>(1, (int64_t)(rounds * cap / (p->C - 1) + 0.999)));
       }
-      // fused blend: a unit's blends trail its fold by about one resident
-      // grid of items (RAVNEST_B200_BLEND_LAG: groups of C items, tuning)
-      lane.blend_lag = ((int64_t)p->sm_count * p->occ + p->C - 1) / p->C;
+      // fused blend: a unit's blends trail its fold by about two resident
+      // grids of items (RAVNEST_B200_BLEND_LAG: groups of C items, tuning;
+      // GPT-2 at 4 GPUs, 1 / 2 / 4 / 8 / 16 grids: 3.53 / 3.22 / 3.28 /
+      // 3.47 / 3.77 ms per cycle + blend)
+      lane.blend_lag = (2 * (int64_t)p->sm_count * p->occ + p->C - 1) / p->C;
       if (const char *be = getenv("RAVNEST_B200_BLEND_LAG")) lane.blend_lag = std::max(0, atoi(be));
       lane.n_tiles = ll ? (int64_t)(p->C - 1) * lane.scatter_umax * 2 + lane.ounits[p->rank]
                         : (int64_t)(p->fused_blend ? 2 * p->C - 1 : p->C) * lane.umax_all;
