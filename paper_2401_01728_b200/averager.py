@@ -13,8 +13,9 @@ still in flight then land their (stale) updates on the averaged parameters
 
 so the tau updates made while the cycle ran are applied on top of the
 average, exactly the reference's stale-update semantics with staleness tau.
-With tau = 0 the blend writes the mean itself (live == snap), i.e. the
-reference's synchronous snapshot barrier.  The cycle is one kernel per rank
+With tau = 0 the cycle writes the mean straight into live (the blend would
+write exactly the mean, live == snap), i.e. the reference's synchronous
+snapshot barrier.  The cycle is one kernel per rank
 (DistRingGroup); with ``graph=True`` it is captured once in a CUDA graph and
 replayed every kappa updates.
 
@@ -52,7 +53,9 @@ class AsyncAverager:
             raise ConfigError(f"tau must be in [0, kappa), got {tau}")
         self.live = live
         self.snap = torch.empty_like(live)
-        self.mean = torch.empty_like(live)
+        # tau = 0: nothing lands on live during the cycle, so the means go
+        # straight into live (the blend would write exactly the mean there)
+        self.mean = live if tau == 0 else torch.empty_like(live)
         self.kappa, self.tau = kappa, tau
         self.train_stream = train_stream or torch.cuda.current_stream(live.device)
         self.avg_stream = torch.cuda.Stream(device=live.device, priority=-1)
@@ -97,7 +100,8 @@ class AsyncAverager:
     def _finish(self):
         self.before_update()
         self.train_stream.wait_event(self._done)
-        blend_(self.live, self.snap, self.mean, self.train_stream)
+        if self.tau > 0:
+            blend_(self.live, self.snap, self.mean, self.train_stream)
         self._pending_at = None
         self.cycles += 1
 
