@@ -58,8 +58,16 @@ All lines are `bench.py` output; raw JSON in `final/*.jsonl`.
 | run | value GB/s | ms/step | bus GB/s per GPU | roofline frac | pattern | e2e GB/s | NCCL bus GB/s | transport |
 |---|---|---|---|---|---|---|---|---|
 """
+    notes = """
+Notes:
+- `*_gpt2_blend` is config 4: snapshot average + τ=4 delayed-update blend per step, the blend fused into the
+  cycle (`rv_plan_bind_live`). Its value uses the whole step; at N=1 the roofline counts the fused kernel's
+  4·C·S bytes, at N>1 the NVLink bytes of the cycle.
+- `lanes 4` is one launch and stream per ring (the north star's layout).
+- `pytest_gpu.log`: the GPU test suite of the same session.
+"""
     with open(out, "w") as f:
-        f.write(head + "\n".join(rows) + "\n")
+        f.write(head + "\n".join(rows) + "\n" + notes)
 
 
 if __name__ == "__main__":
