@@ -275,10 +275,20 @@ int build_tables(rv_plan *p) {
   if (n_live != 0 && n_live != (int)p->local.size())
     return set_err(RV_E_ARG, "live buffers bound on %d of %d local positions", n_live, (int)p->local.size());
   p->blend = n_live > 0;
-  if (p->blend)
-    for (int pos : p->local)
-      if (p->dst[pos] == p->src[pos] || p->live[pos] == p->src[pos] || p->live[pos] == p->dst[pos])
-        return set_err(RV_E_ARG, "blend at position %d needs distinct snapshot, mean and live buffers", pos);
+  if (p->blend) {
+    // every snapshot, mean and live vector its own buffer (start addresses)
+    std::vector<std::pair<uintptr_t, int>> starts;
+    for (int i = 0; i < p->C; ++i) {
+      starts.push_back({(uintptr_t)p->src[i], i});
+      starts.push_back({(uintptr_t)p->dst[i], i});
+      if (p->live[i]) starts.push_back({(uintptr_t)p->live[i], i});
+    }
+    std::sort(starts.begin(), starts.end());
+    for (size_t j = 1; j < starts.size(); ++j)
+      if (starts[j].first == starts[j - 1].first)
+        return set_err(RV_E_ARG, "blend needs distinct snapshot, mean and live buffers (positions %d and %d share one)",
+                       starts[j - 1].second, starts[j].second);
+  }
   const int N = vec ? 16 / es : 1;
   const int64_t a0 = vec ? (int64_t)(a / es) : 0;
   p->ptrs_dirty = false;

@@ -230,6 +230,7 @@ class LocalRingGroup:
             if not (s.is_contiguous() and d.is_contiguous()):
                 raise LayoutError(f"cluster position {m} tensor must be contiguous")
             self.bind(m, s.data_ptr(), d.data_ptr())
+        self._bound = (list(srcs), list(dsts))  # the plans hold raw pointers: keep the tensors alive
 
     def bind_live(self, lives: Sequence | None) -> None:
         """Delayed-update blend fused into the cycle: ``lives[m]`` (a tensor
@@ -245,6 +246,7 @@ class LocalRingGroup:
             for d, plan in self.plans.items():
                 if d == self.devices[m]:
                     plan.bind_live(m, ptr)
+        self._lives = None if lives is None else list(lives)
 
     def run(self, streams: dict | None = None) -> None:
         """Launch one cycle.  ``streams`` maps device -> stream (or a list of

@@ -13,10 +13,17 @@ from paper_2401_01728_b200.plan import LocalRingGroup  # noqa: E402
 
 lens = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "bert"]
 proto = sys.argv[2] if len(sys.argv) > 2 else "pull"
+blend = len(sys.argv) > 3 and sys.argv[3] == "blend"  # fused delayed-update blend
 total = sum(lens)
 xs = [synth(total, m, torch.device(f"cuda:{m}")) for m in range(2)]
 g = LocalRingGroup(ring_starts(lens), lens, total, [0, 1], torch.float32, protocol=proto)
-g.bind_tensors(xs)
+if blend:
+    means = [torch.empty_like(x) for x in xs]  # held: the plan keeps raw pointers
+    lives = [x + 1e-3 for x in xs]
+    g.bind_tensors(xs, means)
+    g.bind_live(lives)
+else:
+    g.bind_tensors(xs)
 streams = {d: torch.cuda.Stream(device=d) for d in (0, 1)}
 for _ in range(5):
     g.run(streams)
