@@ -28,8 +28,14 @@ template <typename T, typename Acc, int VB>
 KernelFn pick_cb(int c, bool push, int *u_out) {
   constexpr bool wide = sizeof(T) == 8;
   if (push) {
-    if (c <= 2) { *u_out = 4; return ring_push_kernel<T, Acc, 2, VB, 4>; }
-    if (c <= 4) { *u_out = 2; return ring_push_kernel<T, Acc, 4, VB, 2>; }
+    // fp64 storage: half again (the blend items' addresses stay in registers)
+    if constexpr (wide) {
+      if (c <= 2) { *u_out = 2; return ring_push_kernel<T, Acc, 2, VB, 2>; }
+      if (c <= 4) { *u_out = 1; return ring_push_kernel<T, Acc, 4, VB, 1>; }
+    } else {
+      if (c <= 2) { *u_out = 4; return ring_push_kernel<T, Acc, 2, VB, 4>; }
+      if (c <= 4) { *u_out = 2; return ring_push_kernel<T, Acc, 4, VB, 2>; }
+    }
     if (c <= 8) { *u_out = 1; return ring_push_kernel<T, Acc, 8, VB, 1>; }
     *u_out = 1;
     return ring_push_kernel<T, Acc, 16, VB, 1>;
