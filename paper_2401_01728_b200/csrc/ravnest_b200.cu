@@ -544,6 +544,11 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
     cp.live_me = p->fused_blend ? p->live[p->rank] : nullptr;
     cp.mflag_off = p->mflag_off;
     cp.blend_lag = lane.blend_lag;
+    cp.blend_blocks = 0;
+    if (p->fused_blend) {
+      const char *bb = getenv("RAVNEST_B200_BLEND_BLOCKS");  // tuning
+      if (bb) cp.blend_blocks = std::max(0, std::min(atoi(bb), std::max(1, lane.grid) - 1));
+    }
     cp.unit_vecs = lane.unit_vecs;
   }
   if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet

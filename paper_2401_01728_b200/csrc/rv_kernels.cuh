@@ -92,6 +92,50 @@ __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
   return segs[a];
 }
 
+// Push with the fused blend: unit u of owner q, once q's mean-delivered flag
+// for it is set: live <- mean + (live - snap) over the unit's range of this
+// rank's buffers.  False when the cycle failed (block must stop).
+template <typename T, int VB>
+__device__ bool blend_item(const CycleParams &p, int q, int64_t u, unsigned long long epoch, unsigned long long t0,
+                           int *s_ok) {
+  constexpr int N = VB / sizeof(T);
+  using Raw = typename RawVec<VB>::type;
+  const int C = p.C, me = p.me;
+  if (u < 0 || u >= p.ounits[q]) return true;
+  const Seg s = find_unit<T>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
+  if (threadIdx.x == 0) {
+    const unsigned diag = (3u << 16) | ((unsigned)p.lane << 8) | (unsigned)q;
+    if (!wait_flag(p, p.pflags[me] + p.mflag_off + pflag_index(p.lane, C, q, p.units_max, u), epoch, t0, diag))
+      *s_ok = 0;
+  }
+  __syncthreads();
+  if (!*s_ok) return false;
+  const int64_t uu = u - s.unit0;
+  const int64_t nvec = (s.body_hi - s.body_lo) / N;
+  const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
+  const T *mean = static_cast<const T *>(p.dst[me]);
+  const T *snap = static_cast<const T *>(p.src[me]);
+  T *live = static_cast<T *>(p.live_me);
+  for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
+    const int64_t i = s.body_lo + j * N;
+    Lanes<T, VB> m, l, sn;
+    m.raw = __ldcg(reinterpret_cast<const Raw *>(mean + i));
+    sn.raw = __ldcs(reinterpret_cast<const Raw *>(snap + i));
+    l.raw = *reinterpret_cast<const Raw *>(live + i);
+#pragma unroll
+    for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(m.v[e], l.v[e], sn.v[e]);
+    *reinterpret_cast<Raw *>(live + i) = l.raw;
+  }
+  if (uu == 0) {
+    const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
+    if ((int64_t)threadIdx.x < nhead + ntail) {
+      const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x : s.body_hi + ((int64_t)threadIdx.x - nhead);
+      live[i] = blend_one<T>(__ldcg(mean + i), live[i], snap[i]);
+    }
+  }
+  return true;
+}
+
 template <typename T, typename Acc, int CB, int VB, int U>
 __global__ void __launch_bounds__(kThreads, 2)
 ring_push_kernel(const __grid_constant__ CycleParams p) {
@@ -118,62 +162,45 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
   // other owners (each waits for that owner's mean-delivered flag, set by a
   // fold item blend_lag groups earlier), so the blend's HBM traffic runs
   // under the NVLink traffic of later folds and finds the means in L2.
+  // RAVNEST_B200_BLEND_BLOCKS > 0 (tuning): the last blend_blocks blocks
+  // take only blend items (unit-major, from their own counter) and the
+  // others the scatter and fold items.
   const int64_t ua = p.umax_all;
   const bool fused = p.live_me != nullptr;
+  const unsigned long long t0 = globaltimer();
+  __shared__ long long s_next;
+  const int nb = fused ? p.blend_blocks : 0;
+  const int n_main = (int)gridDim.x - nb;
+  if (nb > 0 && (int)blockIdx.x >= n_main) {
+    const int64_t n_blend = ua * (C - 1);
+    for (int64_t b = blockIdx.x - n_main; b < n_blend; b = grab_next(p, &s_next, &p.state->grab2, nb)) {
+      if (!s_ok) break;
+      const int r = (int)(b % (C - 1));
+      if (!blend_item<T, VB>(p, me + 1 + r < C ? me + 1 + r : me + 1 + r - C, b / (C - 1), epoch, t0, &s_ok)) break;
+    }
+    depart(p, epoch, false);
+    return;
+  }
+  const bool mixed = fused && nb == 0;  // blend items interleaved with the folds
   const int64_t lag = fused ? ua : p.push_lag, blag = p.blend_lag;
   const int64_t head = lag * (C - 1), n_mix = (ua - lag) * C;
-  const int64_t n_work = fused ? head + (ua + blag) * C : ua * C;
-  const unsigned long long t0 = globaltimer();
+  const int64_t n_work = mixed ? head + (ua + blag) * C : ua * C;
 
-  __shared__ long long s_next;
-  for (int64_t w = blockIdx.x; w < n_work; w = p.push_dyn ? grab_next(p, &s_next) : w + gridDim.x) {
+  for (int64_t w = blockIdx.x; w < n_work;
+       w = p.push_dyn ? grab_next(p, &s_next, &p.state->grab, n_main) : w + n_main) {
     if (!s_ok) break;
     int64_t sidx = -1, fidx = -1;  // scatter item (unit * (C-1) + peer) or fold unit
-    if (fused && w >= head && (w - head) % C != 0) {
+    if (mixed && w >= head && (w - head) % C != 0) {
       // blend item: unit u of owner q, from q's means in this rank's dst
       const int r = (int)((w - head) % C) - 1;
       const int64_t u = (w - head) / C - blag;
-      int q = me + 1 + r;
-      if (q >= C) q -= C;
-      if (u < 0 || u >= p.ounits[q]) continue;
-      const Seg s = find_unit<T>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
-      if (threadIdx.x == 0) {
-        const unsigned diag = (3u << 16) | ((unsigned)p.lane << 8) | (unsigned)q;
-        if (!wait_flag(p, p.pflags[me] + p.mflag_off + pflag_index(p.lane, C, q, p.units_max, u), epoch, t0, diag))
-          s_ok = 0;
-      }
-      __syncthreads();
-      if (!s_ok) break;
-      const int64_t uu = u - s.unit0;
-      const int64_t nvec = (s.body_hi - s.body_lo) / N;
-      const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
-      const T *mean = static_cast<const T *>(p.dst[me]);
-      const T *snap = static_cast<const T *>(p.src[me]);
-      T *live = static_cast<T *>(p.live_me);
-      for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
-        const int64_t i = s.body_lo + j * N;
-        Lanes<T, VB> m, l, sn;
-        m.raw = __ldcg(reinterpret_cast<const Raw *>(mean + i));
-        sn.raw = __ldcs(reinterpret_cast<const Raw *>(snap + i));
-        l.raw = *reinterpret_cast<const Raw *>(live + i);
-#pragma unroll
-        for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(m.v[e], l.v[e], sn.v[e]);
-        *reinterpret_cast<Raw *>(live + i) = l.raw;
-      }
-      if (uu == 0) {
-        const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
-        if ((int64_t)threadIdx.x < nhead + ntail) {
-          const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
-                                                          : s.body_hi + ((int64_t)threadIdx.x - nhead);
-          live[i] = blend_one<T>(__ldcg(mean + i), live[i], snap[i]);
-        }
-      }
+      if (!blend_item<T, VB>(p, me + 1 + r < C ? me + 1 + r : me + 1 + r - C, u, epoch, t0, &s_ok)) break;
       continue;
     }
     if (w < head) {
       sidx = w;
     } else if (fused) {
-      fidx = (w - head) / C;  // j == 0 of group g
+      fidx = mixed ? (w - head) / C : w - head;  // mixed: j == 0 of group g
     } else if (w - head < n_mix) {
       const int64_t f = (w - head) / C, j = (w - head) % C;
       if (j == 0) fidx = f; else sidx = (f + lag) * (C - 1) + (j - 1);
