@@ -128,6 +128,7 @@ struct rv_plan {
   size_t smem_bytes = 0;
   int max_blocks = 0;  // 0 = whole device; else cap on resident blocks (SM budget)
   int push_dyn = 1;    // push: work items from a counter (RAVNEST_B200_PUSH_DYN=0: static stride)
+  int blend_blocks = 0;  // push, fused blend: blend-only blocks (RAVNEST_B200_BLEND_BLOCKS, tuning)
   bool blend = false;        // live bound on the local positions: every cycle ends with the blend
   bool fused_blend = false;  // ... inside the push kernel (else blend launches after each lane)
   int64_t mflag_off = 0;     // push: mean-delivered flags after the scatter flags (u64 index)
@@ -309,6 +310,8 @@ int build_tables(rv_plan *p) {
   {
     const char *de = getenv("RAVNEST_B200_PUSH_DYN");  // tuning
     p->push_dyn = de ? atoi(de) != 0 : 1;
+    const char *bb = getenv("RAVNEST_B200_BLEND_BLOCKS");  // tuning
+    p->blend_blocks = bb ? std::max(0, atoi(bb)) : 0;
   }
   const bool ll = ll_active(p);
   if (ll && p->dtype != RV_DTYPE_F32) return set_err(RV_E_CONFIG, "the LL transport carries fp32 parameters only");
@@ -544,11 +547,7 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
     cp.live_me = p->fused_blend ? p->live[p->rank] : nullptr;
     cp.mflag_off = p->mflag_off;
     cp.blend_lag = lane.blend_lag;
-    cp.blend_blocks = 0;
-    if (p->fused_blend) {
-      const char *bb = getenv("RAVNEST_B200_BLEND_BLOCKS");  // tuning
-      if (bb) cp.blend_blocks = std::max(0, std::min(atoi(bb), std::max(1, lane.grid) - 1));
-    }
+    cp.blend_blocks = p->fused_blend ? std::min(p->blend_blocks, std::max(1, lane.grid) - 1) : 0;
     cp.unit_vecs = lane.unit_vecs;
   }
   if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet
