@@ -893,7 +893,7 @@ int rv_plan_status(rv_plan *p, char *diag, size_t diag_len) {
   std::string rings;
   if (lane < p->lanes.size())
     for (int r : p->lanes[lane].rings) rings += (rings.empty() ? "" : "|") + std::to_string(r);
-  const char *ph = phase == 0 ? "arrive" : phase == 1 ? "depart" : "unit";
+  const char *ph = phase == 0 ? "arrive" : phase == 1 ? "depart" : phase == 2 ? "unit" : "mean-delivered";
   if (diag && diag_len)
     snprintf(diag, diag_len, "waiting on: (ring=%s, phase=%s, rank=%u)", rings.empty() ? "?" : rings.c_str(), ph,
              peer);

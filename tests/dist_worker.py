@@ -30,9 +30,13 @@ def stall_phase(rank, world, local):
     failures = 0
     lens = [4097, 333]
     total = sum(lens)
-    for proto in ("pull", "push", "ll"):
+    for proto in ("pull", "push", "ll", "push+blend"):
+        blend = proto.endswith("+blend")
+        proto = proto.split("+")[0]
         x = torch.full((total,), float(rank), device=f"cuda:{local}")
-        g = DistRingGroup(src=x, starts=[0, lens[0]], lens=lens, protocol=proto, timeout_s=0.5)
+        mean = torch.empty_like(x) if blend else None
+        live = torch.zeros_like(x) if blend else None
+        g = DistRingGroup(src=x, dst=mean, starts=[0, lens[0]], lens=lens, protocol=proto, timeout_s=0.5, live=live)
         if rank == 0:
             g.average()
             torch.cuda.synchronize()
