@@ -94,8 +94,20 @@ def blend_phase(rank, world, local):
             streams = [torch.cuda.Stream() for _ in range(lanes)]
             for st in streams:
                 st.wait_stream(torch.cuda.current_stream())
-            for _ in range(3):
+            if lanes == 1 and dt == torch.float32:
+                # one cycle, then two CUDA-graph replays of a captured cycle
+                # (device-side epochs, work counters and flags are graph-safe)
                 g.average(streams)
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=streams[0]):
+                    g.average(streams)
+                dist.barrier()
+                for _ in range(2):
+                    graph.replay()
+            else:
+                for _ in range(3):
+                    g.average(streams)
             torch.cuda.synchronize()
             g.check()
             want_mean = ring_oracle.ring_mean(starts, lens, snaps)[rank].astype(npdt)
