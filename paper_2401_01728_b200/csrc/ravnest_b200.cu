@@ -116,7 +116,7 @@ struct rv_plan {
     std::vector<int> rings;  // rings meeting the range
     int grid = 0;
     // push
-    int64_t stride = 0, unit_vecs = 0, scatter_umax = 0, umax_all = 0, push_lag = 0, blend_lag = 0;
+    int64_t stride = 0, unit_vecs = 0, scatter_umax = 0, umax_all = 0, blend_lag = 0;
     std::vector<int64_t> ounits;
     std::vector<int> oseg_base;
   };
@@ -128,7 +128,6 @@ struct rv_plan {
   size_t smem_bytes = 0;
   int max_blocks = 0;  // 0 = whole device; else cap on resident blocks (SM budget)
   int push_dyn = 1;    // push: work items from a counter (RAVNEST_B200_PUSH_DYN=0: static stride)
-  int blend_blocks = 0;  // push, fused blend: blend-only blocks (RAVNEST_B200_BLEND_BLOCKS, tuning)
   bool blend = false;        // live bound on the local positions: every cycle ends with the blend
   bool fused_blend = false;  // ... inside the push kernel (else blend launches after each lane)
   int64_t mflag_off = 0;     // push: mean-delivered flags after the scatter flags (u64 index)
@@ -310,8 +309,6 @@ int build_tables(rv_plan *p) {
   {
     const char *de = getenv("RAVNEST_B200_PUSH_DYN");  // tuning
     p->push_dyn = de ? atoi(de) != 0 : 1;
-    const char *bb = getenv("RAVNEST_B200_BLEND_BLOCKS");  // tuning
-    p->blend_blocks = bb ? std::max(0, atoi(bb)) : 0;
   }
   const bool ll = ll_active(p);
   if (ll && p->dtype != RV_DTYPE_F32) return set_err(RV_E_CONFIG, "the LL transport carries fp32 parameters only");
@@ -451,18 +448,6 @@ int build_tables(rv_plan *p) {
         if (q != p->rank) lane.scatter_umax = std::max(lane.scatter_umax, lane.ounits[q]);
         lane.umax_all = std::max(lane.umax_all, lane.ounits[q]);
       }
-      // fold items start after `lag` units' scatters: that many rounds of
-      // the resident grid (RAVNEST_B200_PUSH_LAG, in rounds; default: every
-      // scatter first).  Derived from the schedule and the device model
-      // only, so every rank uses the same work order.
-      lane.push_lag = lane.umax_all;
-      if (const char *le = getenv("RAVNEST_B200_PUSH_LAG")) {
-        const double rounds = atof(le);
-        const int64_t cap = (int64_t)p->sm_count * p->occ;
-        if (rounds > 0)
-          lane.push_lag = std::min<int64_t>(lane.umax_all,
-                                            std::max<int64_t>(1, (int64_t)(rounds * cap / (p->C - 1) + 0.999)));
-      }
       // fused blend: a unit's blends trail its fold by about two resident
       // grids of items (RAVNEST_B200_BLEND_LAG: groups of C items, tuning;
       // GPT-2 at 4 GPUs, 1 / 2 / 4 / 8 / 16 grids: 3.53 / 3.22 / 3.28 /
@@ -542,12 +527,10 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
     cp.units_max = p->units_max;
     cp.scatter_umax = lane.scatter_umax;
     cp.umax_all = lane.umax_all;
-    cp.push_lag = lane.push_lag;
     cp.push_dyn = p->push_dyn;
     cp.live_me = p->fused_blend ? p->live[p->rank] : nullptr;
     cp.mflag_off = p->mflag_off;
     cp.blend_lag = lane.blend_lag;
-    cp.blend_blocks = p->fused_blend ? std::min(p->blend_blocks, std::max(1, lane.grid) - 1) : 0;
     cp.unit_vecs = lane.unit_vecs;
   }
   if (lane.n_tiles == 0 && p->n_ranks == 1) return RV_OK;  // nothing to fold, nobody to meet

@@ -62,8 +62,6 @@ struct LaneState {
   unsigned long long signaled;  // last epoch whose arrive flags were posted
   unsigned int done;            // blocks finished in the running cycle
   unsigned int grab;            // push: work items handed out beyond the first one per block
-  unsigned int grab2;           // push: the same for the blend-only blocks
-  unsigned int pad;
 };
 
 struct CycleParams {
@@ -83,13 +81,11 @@ struct CycleParams {
   int64_t units_max;           // push: unit-flag slots per (lane, writer)
   int64_t scatter_umax;        // push: max units over the other owners
   int64_t umax_all;            // push: max units over every owner (same on every rank)
-  int64_t push_lag;            // push: units scattered before the first fold item (1..umax_all)
   int push_dyn;                // push: blocks take work items from a counter (else stride by grid)
   void *live[RV_MAX_CLUSTERS]; // co-resident (TMA), fused blend: every member's live buffer
   void *live_me;               // push, fused blend: this rank's live buffer (else NULL)
   int64_t mflag_off;           // push, fused blend: mean-delivered flags, offset in a push area's flags
   int64_t blend_lag;           // push, fused blend: groups between a fold item and the blends of its unit
-  int blend_blocks;            // push, fused blend: blocks that take only blend items (0: interleaved)
   int64_t unit_vecs;           // push: vectors per unit
   int64_t ounits[RV_MAX_CLUSTERS];
   int oseg_base[RV_MAX_CLUSTERS + 1];
@@ -172,10 +168,9 @@ __device__ __forceinline__ void trace_max(const CycleParams &p, int slot) {
 // Next work item of a block: the items go out in position order, each block
 // taking a new one when it finishes its last (the first item of block b is
 // b).  Uniform across the block.
-__device__ __forceinline__ int64_t grab_next(const CycleParams &p, long long *s_next, unsigned int *counter,
-                                             int n_blocks) {
+__device__ __forceinline__ int64_t grab_next(const CycleParams &p, long long *s_next) {
   __syncthreads();
-  if (threadIdx.x == 0) *s_next = (long long)n_blocks + (long long)atomicAdd(counter, 1u);
+  if (threadIdx.x == 0) *s_next = (long long)gridDim.x + (long long)atomicAdd(&p.state->grab, 1u);
   __syncthreads();
   return *s_next;
 }
@@ -200,7 +195,6 @@ __device__ void depart(const CycleParams &p, unsigned long long epoch, bool cros
       trace_max(p, 3);
       p.state->done = 0u;
       p.state->grab = 0u;
-      p.state->grab2 = 0u;
       *(volatile unsigned long long *)&p.state->epoch = epoch;
       __threadfence();
     }

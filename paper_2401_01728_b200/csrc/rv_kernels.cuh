@@ -153,59 +153,38 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
   __syncthreads();
   const unsigned long long epoch = s_epoch;
   const int C = p.C, me = p.me;
-  // Work order (identical on every rank): the scatter items of the first
-  // `lag` units, then one fold item per C - 1 further scatter items, then
-  // the remaining folds.  A fold item only waits on peers' scatter items at
-  // earlier positions, so a co-resident grid always drains.
-  // With the fused blend: every scatter item, then groups of C items, group
-  // g = fold unit g, then the blend items of unit g - blend_lag of the C - 1
-  // other owners (each waits for that owner's mean-delivered flag, set by a
-  // fold item blend_lag groups earlier), so the blend's HBM traffic runs
-  // under the NVLink traffic of later folds and finds the means in L2.
-  // RAVNEST_B200_BLEND_BLOCKS > 0 (tuning): the last blend_blocks blocks
-  // take only blend items (unit-major, from their own counter) and the
-  // others the scatter and fold items.
+  // Work order (identical on every rank): every scatter item (unit-major),
+  // then every fold item.  With the fused blend the folds come in groups of
+  // C items: group g = fold unit g, then the blend items of unit
+  // g - blend_lag of the C - 1 other owners (each waits for that owner's
+  // mean-delivered flag, set by a fold item blend_lag groups earlier), so
+  // the blend's HBM traffic runs under the NVLink traffic of later folds
+  // and finds the means in L2.  Items wait only on items at earlier
+  // positions (of other ranks), and blocks take items in position order,
+  // so a co-resident grid always drains.
   const int64_t ua = p.umax_all;
   const bool fused = p.live_me != nullptr;
+  const int64_t blag = p.blend_lag;
+  const int64_t head = ua * (C - 1);
+  const int64_t n_work = fused ? head + (ua + blag) * C : ua * C;
   const unsigned long long t0 = globaltimer();
   __shared__ long long s_next;
-  const int nb = fused ? p.blend_blocks : 0;
-  const int n_main = (int)gridDim.x - nb;
-  if (nb > 0 && (int)blockIdx.x >= n_main) {
-    const int64_t n_blend = ua * (C - 1);
-    for (int64_t b = blockIdx.x - n_main; b < n_blend; b = grab_next(p, &s_next, &p.state->grab2, nb)) {
-      if (!s_ok) break;
-      const int r = (int)(b % (C - 1));
-      if (!blend_item<T, VB>(p, me + 1 + r < C ? me + 1 + r : me + 1 + r - C, b / (C - 1), epoch, t0, &s_ok)) break;
-    }
-    depart(p, epoch, false);
-    return;
-  }
-  const bool mixed = fused && nb == 0;  // blend items interleaved with the folds
-  const int64_t lag = fused ? ua : p.push_lag, blag = p.blend_lag;
-  const int64_t head = lag * (C - 1), n_mix = (ua - lag) * C;
-  const int64_t n_work = mixed ? head + (ua + blag) * C : ua * C;
 
-  for (int64_t w = blockIdx.x; w < n_work;
-       w = p.push_dyn ? grab_next(p, &s_next, &p.state->grab, n_main) : w + n_main) {
+  for (int64_t w = blockIdx.x; w < n_work; w = p.push_dyn ? grab_next(p, &s_next) : w + gridDim.x) {
     if (!s_ok) break;
     int64_t sidx = -1, fidx = -1;  // scatter item (unit * (C-1) + peer) or fold unit
-    if (mixed && w >= head && (w - head) % C != 0) {
+    if (w < head) {
+      sidx = w;
+    } else if (!fused) {
+      fidx = w - head;
+    } else if ((w - head) % C == 0) {
+      fidx = (w - head) / C;
+    } else {
       // blend item: unit u of owner q, from q's means in this rank's dst
       const int r = (int)((w - head) % C) - 1;
       const int64_t u = (w - head) / C - blag;
       if (!blend_item<T, VB>(p, me + 1 + r < C ? me + 1 + r : me + 1 + r - C, u, epoch, t0, &s_ok)) break;
       continue;
-    }
-    if (w < head) {
-      sidx = w;
-    } else if (fused) {
-      fidx = mixed ? (w - head) / C : w - head;  // mixed: j == 0 of group g
-    } else if (w - head < n_mix) {
-      const int64_t f = (w - head) / C, j = (w - head) % C;
-      if (j == 0) fidx = f; else sidx = (f + lag) * (C - 1) + (j - 1);
-    } else {
-      fidx = (ua - lag) + (w - head - n_mix);
     }
     if (sidx >= 0) {
       const int r = (int)(sidx % (C - 1));

@@ -1,4 +1,5 @@
 # fused blend: blend items interleaved (0) vs a dedicated set of blend-only blocks
+# historical: the kernel variant this measured was removed afterwards (DESIGN.md tuning table); the knob is now ignored
 export RAVNEST_B200_TIMEOUT_S=10
 RAVNEST_B200_BLEND_BLOCKS=64 RAVNEST_DIST_QUICK=1 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29670 tests/dist_worker.py 2>&1 | grep "DIST"
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"

@@ -1,4 +1,5 @@
 # push work distribution: static stride vs a work counter, with and without interleaved folds
+# historical: RAVNEST_B200_PUSH_LAG (fold interleaving) was removed afterwards; only the PUSH_DYN legs still apply
 export RAVNEST_B200_TIMEOUT_S=10
 for d in 1; do
 RAVNEST_B200_PUSH_DYN=$d RAVNEST_DIST_QUICK=1 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29630 tests/dist_worker.py 2>&1 | grep "DIST"

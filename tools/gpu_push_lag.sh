@@ -1,4 +1,5 @@
 # push work order: fold items interleaved after a lag of N resident-grid rounds
+# historical: the kernel variant this measured was removed afterwards (DESIGN.md tuning table); the knob is now ignored
 RAVNEST_B200_PUSH_LAG=1 RAVNEST_DIST_QUICK=1 RAVNEST_B200_TIMEOUT_S=10 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29620 tests/dist_worker.py 2>&1 | grep "DIST" 
 RAVNEST_B200_PUSH_LAG=0.3 RAVNEST_DIST_QUICK=1 RAVNEST_B200_TIMEOUT_S=10 python -m torch.distributed.run --nnodes=1 --nproc-per-node 3 --master-addr 127.0.0.1 --master-port 29621 tests/dist_worker.py 2>&1 | grep "DIST"
 for wl in resnet50 bert; do
