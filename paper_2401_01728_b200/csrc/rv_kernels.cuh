@@ -517,15 +517,34 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
   }
   __syncthreads();
 
-  // the tiles this block owns: t = blockIdx.x + i * gridDim.x
-  auto seg_of = [&](int64_t t, int64_t *local) -> Seg {
-    int a = 0, b = p.nseg - 1;
-    while (a < b) {
-      const int mid = (a + b + 1) >> 1;
-      if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
+  // the tiles this block owns: t = blockIdx.x + i * gridDim.x, increasing,
+  // so each thread walks the segment table forward from its last segment
+  // (one binary search for the first tile) and reloads the chunk record only
+  // when the segment changes
+  int seg_a = -1;
+  int64_t seg_next = 0, seg_base = 0;  // tile_prefix[seg_a + 1], tile_prefix[seg_a]
+  Seg seg_cur;
+  auto seg_of = [&](int64_t t, int64_t *local) -> const Seg & {
+    if (seg_a < 0) {
+      int a = 0, b = p.nseg - 1;
+      while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
+      }
+      seg_a = a;
+      seg_base = __ldg(p.tile_prefix + a);
+      seg_next = __ldg(p.tile_prefix + a + 1);
+      seg_cur = p.segs[a];
+    } else if (t >= seg_next) {
+      int a = seg_a + 1;
+      while (__ldg(p.tile_prefix + a + 1) <= t) ++a;
+      seg_a = a;
+      seg_base = __ldg(p.tile_prefix + a);
+      seg_next = __ldg(p.tile_prefix + a + 1);
+      seg_cur = p.segs[a];
     }
-    *local = t - __ldg(p.tile_prefix + a);
-    return p.segs[a];
+    *local = t - seg_base;
+    return seg_cur;
   };
 
   if (tid < 32) {
