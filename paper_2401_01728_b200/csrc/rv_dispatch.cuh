@@ -137,7 +137,7 @@ KernelFn pick_tma_kernel(int mode, int c, bool blend, int *tv_out, size_t *smem_
                            : pick_tma<double, double, kTmaStages, kTmaStageBytes>(c, tv_out);
   }
   const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
-  *smem_out = (size_t)stages * cb * (*tv_out) * 16 + 2 * (size_t)(*tv_out) * 16;
+  *smem_out = (size_t)stages * cb * (*tv_out) * 16 + 3 * (size_t)(*tv_out) * 16;  // 3 output buffers
   return k;
 }
 

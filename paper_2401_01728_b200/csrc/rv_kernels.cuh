@@ -500,9 +500,10 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = 16 / sizeof(T);
   constexpr int SLOTS = BL ? 2 * CB : CB;  // tiles per stage: src (ring order), then live
   constexpr int OUTS = BL ? CB + 1 : 1;    // output tiles: mean, then blended live
+  constexpr int NOB = BL ? 2 : 3;          // output buffers (bulk-store groups in flight)
   extern __shared__ __align__(128) unsigned char smem[];
   uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][SLOTS][TV]
-  uint4 *out = in + (size_t)STAGES * SLOTS * TV;                       // [2][OUTS][TV]
+  uint4 *out = in + (size_t)STAGES * SLOTS * TV;                       // [NOB][OUTS][TV]
   __shared__ __align__(8) unsigned long long full[STAGES], empty[STAGES];
   const int tid = threadIdx.x;
   const int C = p.C;
@@ -651,7 +652,12 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
           }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // out[ob ^ 1] reusable
+      // the buffer the next tile writes is free once at most NOB - 1 groups
+      // are still reading shared memory
+      if constexpr (NOB == 3)
+        asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+      else
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     }
     if (lt == 0) {
       const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
@@ -665,7 +671,7 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
           }
       }
     }
-    ob ^= 1;
+    if (++ob == NOB) ob = 0;
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1;
