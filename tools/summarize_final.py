@@ -65,6 +65,9 @@ Notes:
   4·C·S bytes, at N>1 the NVLink bytes of the cycle.
 - `lanes 4` is one launch and stream per ring (the north star's layout).
 - `pytest_gpu.log`: the GPU test suite of the same session.
+- `*_rerun*`: a configuration run again in a separate call. When the timed steps are separated by L2 flushes
+  (ResNet-50 at N>1), `ms_per_step` is the mean of the per-step intervals, so one slow step (a rank whose host
+  queued its step late) raises the mean; the line's `ms_per_step_median` / `ms_per_step_min` show it.
 """
     with open(out, "w") as f:
         f.write(head + "\n".join(rows) + "\n" + notes)
