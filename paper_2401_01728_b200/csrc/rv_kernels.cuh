@@ -74,13 +74,16 @@ ring_cycle_kernel(const __grid_constant__ CycleParams p) {
 // ---------------------------------------------------------------------------
 // push protocol (one position per rank, rank == position): NVLink carries
 // stores only.  Scatter: this rank copies its chunk-q slice of every ring into
-// owner q's staging slot and raises one release flag per 256 KB unit.  Fold:
-// for its own chunk, once every writer's flag for a unit is up, the owner
-// folds its own values and the staged ones in ring order and pushes the mean
-// into all members.  No arrive barrier is needed: a member's chunk reaches
-// the owner only after its kernel started (inputs final), and the owner
-// writes a member's buffer only after receiving that member's data for the
-// same unit.  The depart barrier still closes the cycle.
+// owner q's staging slot and raises one release flag per unit (16-256 KB).
+// Fold: for its own chunk, once every writer's flag for a unit is up, the
+// owner folds its own values and the staged ones in ring order and pushes
+// the mean into all members.  No arrive barrier is needed: a member's chunk
+// reaches the owner only after its kernel started (inputs final), and the
+// owner writes a member's buffer only after receiving that member's data for
+// the same unit.  The depart barrier closes the cycle; with the fused blend
+// the owner also raises a mean-delivered flag per unit on every member, each
+// member awaits all of them (its blend items), and no depart barrier is
+// needed.
 
 template <typename T>
 __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
