@@ -44,7 +44,8 @@ WORKLOAD_NAMES = {
     "gpt2": "GPT-2 medium parameter set (354,823,168 fp32), 8 rings",
 }
 METRIC = "param-averaging bus GB/s and ms/round at 1/2/4/8 B200 vs NVLink roofline"
-NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md)
+NVLINK_PEAK_GBS = 900.0  # NVLink 5 per direction per GPU: the roofline north_star / BASELINE.md name
+NVLINK_PEER_COPY_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md), secondary
 # user-data ceilings of each transport's traffic pattern: ~840 GB/s raw per
 # direction / (1 + protocol overhead), ncu-measured (profiles/r01/ncu_nvlink.md)
 PATTERN_CEILING_GBS = {"push": 706.0, "pull": 656.0}
@@ -242,34 +243,120 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def import_reference():
+    """The UNMODIFIED reference package: baseline/_ref (the offline install,
+    travels to the GPU box), else the read-only tree of the dev container.
+    Returns (ravnest module, where) or (None, why)."""
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "ravnest")):
+            sys.dont_write_bytecode = True  # /root/reference is read-only
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            try:
+                import ravnest
+                import ravnest.multiring  # noqa: F401
+            except Exception as e:  # pragma: no cover - broken install
+                return None, f"import from {path} failed: {e!r}"
+            return ravnest, path
+    return None, "baseline/_ref not installed (see DESIGN.md, reference install)"
+
+
+def host_inputs(total: int, c: int):
+    """Per-cluster fp32 N(0, 0.02) vectors, Philox-seeded."""
+    import numpy as np
+
+    return [np.random.Generator(np.random.Philox(key=SEED * 1000 + m)).standard_normal(total, dtype=np.float32)
+            * np.float32(SIGMA) for m in range(c)]
+
+
+def mem_available() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
 def run_reference(args, n_gpus: int, rank: int):
-    """--impl reference: the reference's own algorithm (faithful numpy port of
-    apply_ring_mean, single-threaded like the reference) on a bounded sample
-    of the same workload, rank 0 only."""
+    """--impl reference: the reference's own CPU implementation of the path --
+    the unmodified ``ravnest.multiring.apply_ring_mean`` (multiring.py:302-333)
+    imported from baseline/_ref -- on the FULL workload of our arm (same rings,
+    same C, fp32 N(0, 0.02) inputs that it widens to float64 itself), rank 0
+    only.  One full-size cycle takes seconds, so the step count is capped to
+    keep the arm within a few minutes (``steps`` reports what was timed).
+    Without the install (or the RAM for a full cycle) it falls back to the
+    faithful port on a bounded sample and says so."""
     if rank != 0:
         return
+    import numpy as np
+
     lens = WORKLOADS[args.workload]
     c = args.clusters or (8 if n_gpus == 1 else n_gpus)
-    smp = CpuSample(lens, c, args.ref_sample_params)
-    for _ in range(args.warmup):
-        smp.run_port()
-    steps = [smp.run_port() for _ in range(args.steps)]
-    t = statistics.median(steps)
-    value = busbw(smp.total, c, t) * n_gpus
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
-        "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * 1e3 * sum(lens) / smp.total, 3),
+    total = sum(lens)
+    starts = ring_starts(lens)
+    ravnest, where = import_reference()
+    need = total * c * (4 + 3 * 8)  # fp32 inputs + the reference's float64 working set (SURVEY §8d)
+    full = ravnest is not None and args.ref_sample_params <= 0 and (mem_available() == 0 or need < 0.8 * mem_available())
+    base = {
+        "impl": "reference", "metric": METRIC, "unit": "GB/s", "n_gpus": n_gpus,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference arithmetic)",
-        "data": "synthetic N(0,0.02) fp32 widened to fp64 like the reference, Philox seeded",
+        "data": "synthetic N(0,0.02) fp32 per cluster (Philox seeded), widened to fp64 by the reference",
         "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                    "parallelism": "1 host thread (numpy ufuncs, as the reference)"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-                         "sample": f"first {smp.total} of {sum(lens)} params per cluster (every ring scaled), "
-                                   f"C={c}, round-by-round numpy port of multiring.apply_ring_mean "
-                                   f"(oracle/ring_oracle.ring_mean_rounds), {cpu_model()}"},
-        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if full:
+        mr = ravnest.multiring
+        sched = mr.build_ring_schedule({m: [mr.ParamRange(st, n) for st, n in zip(starts, lens)] for m in range(c)})
+        xs = host_inputs(total, c)
+        vals = {m: xs[m] for m in range(c)}
+        t0 = time.perf_counter()
+        out = mr.apply_ring_mean(sched, vals)  # warm-up (and the step-count estimate)
+        first = time.perf_counter() - t0
+        del out
+        warm = 1
+        for _ in range(min(args.warmup, 2) - 1):
+            if first * (warm + 1) > args.ref_budget_s / 2:
+                break
+            mr.apply_ring_mean(sched, vals)
+            warm += 1
+        steps = max(1, min(args.steps, int(args.ref_budget_s // max(first, 1e-3))))
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            out = mr.apply_ring_mean(sched, vals)
+            times.append(time.perf_counter() - t0)
+            del out
+        t = statistics.median(times)
+        value = busbw(total, c, t) * n_gpus
+        sample = (f"FULL workload: {c} clusters x {total} params, unmodified ravnest.multiring.apply_ring_mean "
+                  f"from {os.path.relpath(where, ROOT) if where.startswith(ROOT) else where}; "
+                  f"{warm} warm-up + {steps} timed cycle(s) of the {args.steps} requested (one cycle takes "
+                  f"{first:.1f} s; capped at ~{args.ref_budget_s:.0f} s), median; {cpu_model()}")
+        line = dict(base, value=round(value, 4), steps=steps, warmup=warm, steps_requested=args.steps,
+                    ms_per_step=round(t * 1e3, 3), ms_per_round=round(t * 1e3 / (2 * (c - 1)), 3),
+                    ms_per_step_min=round(min(times) * 1e3, 3))
+        line["cpu_baseline"] = {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+                                "sample": sample}
+    else:
+        why = where if ravnest is None else ("--ref-sample-params set" if args.ref_sample_params > 0 else
+                                             f"full cycle needs ~{need / 1e9:.0f} GB of host RAM")
+        smp = CpuSample(lens, c, args.ref_sample_params if args.ref_sample_params > 0 else 2_000_000)
+        for _ in range(args.warmup):
+            smp.run_port()
+        times = [smp.run_port() for _ in range(args.steps)]
+        t = statistics.median(times)
+        value = busbw(smp.total, c, t) * n_gpus
+        line = dict(base, value=round(value, 4), steps=args.steps, warmup=args.warmup,
+                    ms_per_step=round(t * 1e3 * total / smp.total, 3), ms_per_step_extrapolated=True)
+        line["cpu_baseline"] = {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                                "sample": f"first {smp.total} of {total} params per cluster (every ring scaled), "
+                                          f"C={c}, round-by-round numpy port of multiring.apply_ring_mean "
+                                          f"(oracle/ring_oracle.ring_mean_rounds); not the full workload: {why}; "
+                                          f"{cpu_model()}"}
+    line["e2e"] = {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
 
 
@@ -476,6 +563,8 @@ def run_single(args):
     plan_e2e.check()
     e2e_ms = a.elapsed_time(b) / e_steps
 
+    seam = optional_leg("e2e_seam", lambda: e2e_seam(lens, c, xs, args.e2e_seam_steps)) if args.e2e_seam else None
+
     peaks = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     # the fused blend also reads and writes every live vector
@@ -486,7 +575,7 @@ def run_single(args):
     # CPU baselines on bounded samples: the reference algorithm (faithful
     # port, 1 thread) and the closed-form C oracle on every host thread
     threads = host_threads()
-    cpu_port, cpu_threaded = cpu_legs(lens, c, args.ref_sample_params, args.cpu_sample_params, threads)
+    cpu_port, cpu_threaded = cpu_legs(lens, c, args.cpu_port_params, args.cpu_sample_params, threads)
 
     line = {
         "metric": METRIC, "value": round(bw, 3), "unit": "GB/s", "n_gpus": 1,
@@ -516,11 +605,64 @@ def run_single(args):
                 "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": c * total * 4, "d2h_bytes_per_step": c * total * 4,
                 "path": f"rv_allreduce_mean_host (pinned host fp32, {args.e2e_lanes} pipelined lanes)"},
+        "e2e_seam": seam,
         "gpu_launches": args.steps * (args.lanes + (0 if in_cycle_blend or not args.blend
                                                      else c * (1 + (1 if total % 4 else 0)))),
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
+
+
+def plan_options(args) -> dict:
+    """rv_plan_set_option values from the command line (kernel-bucket and
+    push-layout experiments; defaults are the library's)."""
+    opts = {}
+    if args.min_cb:
+        opts["min_cb"] = args.min_cb
+    if args.push_items:
+        opts["push_items"] = args.push_items
+    if args.blend_lag >= 0:
+        opts["blend_lag"] = args.blend_lag
+    return opts
+
+
+def e2e_seam(lens, c: int, xs, steps: int):
+    """The reference user's call, end to end: after ``plugin.install`` on the
+    unmodified reference, ``ravnest.multiring.apply_ring_mean(schedule,
+    {cid: float64 numpy})`` (multiring.py:302-333) -- float64 copy-in into
+    pinned staging, H2D, the float64 kernel, D2H, new float64 arrays out,
+    pipelined by lane.  Host wall time per call (the call is synchronous)."""
+    import numpy as np
+
+    ravnest, where = import_reference()
+    if ravnest is None:
+        return {"unavailable": where}
+    from paper_2401_01728_b200 import plugin
+
+    mr = ravnest.multiring
+    total = sum(lens)
+    starts = ring_starts(lens)
+    sched = mr.build_ring_schedule({m: [mr.ParamRange(st, n) for st, n in zip(starts, lens)] for m in range(c)})
+    vals = {m: xs[m].cpu().numpy().astype(np.float64) for m in range(c)}
+    plugin.install(ravnest)
+    try:
+        out = mr.apply_ring_mean(sched, vals)  # warm-up: plan, device buffers, pinned staging
+        ok = bool(np.array_equal(out[0][:4096], out[c - 1][:4096]))
+        del out
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            out = mr.apply_ring_mean(sched, vals)
+            times.append(time.perf_counter() - t0)
+            del out
+    finally:
+        plugin.uninstall(ravnest)
+    t = statistics.median(times)
+    return {"value": round(busbw(total, c, t), 3), "unit": "GB/s", "ms_per_step": round(t * 1e3, 2),
+            "ms_per_step_min": round(min(times) * 1e3, 2), "steps": steps,
+            "h2d_bytes_per_step": c * total * 8, "d2h_bytes_per_step": c * total * 8, "members_agree": ok,
+            "path": "ravnest.multiring.apply_ring_mean after plugin.install (unmodified reference, numpy float64 "
+                    "in/out, float64 kernel bitwise the reference)"}
 
 
 def run_multi(args, rank: int, world: int, local_rank: int):
@@ -545,7 +687,8 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     # kernel, or launched per lane by the C ABI for the other transports
     in_cycle_blend = bool(args.blend and args.fused_blend)
     grp = DistRingGroup(src=x, dst=mean, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.lanes,
-                        protocol=args.protocol, max_blocks=args.max_blocks, live=live if in_cycle_blend else None)
+                        protocol=args.protocol, max_blocks=args.max_blocks, live=live if in_cycle_blend else None,
+                        options=plan_options(args))
     stream = torch.cuda.current_stream()
     lane_streams = [torch.cuda.Stream() for _ in range(args.lanes)] if args.lanes > 1 else None
 
@@ -570,29 +713,41 @@ def run_multi(args, rank: int, world: int, local_rank: int):
     grp.check()
     dist.barrier()
     torch.cuda.synchronize()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
     flush, l2_text = l2_policy(args.l2_flush, total * 4 * (3 if args.blend else 1), dev)
-    a.record(stream)
-    evs = time_steps(step, stream, args.steps, flush)
-    b.record(stream)
+    # every timed step starts from a rank-aligned point: a one-element NCCL
+    # all-reduce on the step's stream (it completes on all ranks together)
+    # right before the step's start event, after the optional L2 flush.  A
+    # step is then timed per rank from that point, and each step's duration
+    # is the max over ranks.
+    align = torch.zeros(1, device=dev)
+    evs = []
+    for _ in range(args.steps):
+        if flush is not None:
+            flush(stream)
+        dist.all_reduce(align)
+        e = tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e[0].record(stream)
+        step(e[1])
+        e[2].record(stream)
+        evs.append(e)
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop() if clocks else None
     grp.check()
-    kern_local = statistics.mean(ea.elapsed_time(em) for ea, em, _ in evs)
-    per_step = [ea.elapsed_time(eb) for ea, _, eb in evs]
-    ms_local = a.elapsed_time(b) / args.steps if flush is None else statistics.mean(per_step)
-    t = torch.tensor([ms_local, kern_local, statistics.median(per_step), min(per_step)], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # gloo, outside the timed region
-    ms, kernel_ms, step_median, step_min = (float(v) for v in t)
+    per = torch.tensor([[ea.elapsed_time(eb) for ea, _, eb in evs], [ea.elapsed_time(em) for ea, em, _ in evs]],
+                       dtype=torch.float64)
+    dist.all_reduce(per, op=dist.ReduceOp.MAX)  # per step, max over ranks (gloo, outside the timed region)
+    per_step, per_kernel = per[0].tolist(), per[1].tolist()
+    ms, kernel_ms = statistics.mean(per_step), statistics.mean(per_kernel)
+    step_median, step_min = statistics.median(per_step), min(per_step)
+    kernel_median = statistics.median(per_kernel)
 
     # e2e through the host-buffer C ABI: pinned host -> GPU -> average -> host
     numa_cpus = bind_to_gpu_numa(local_rank) if args.numa_bind else ""
     hsrc = x.cpu().pin_memory()
     hdst = torch.empty_like(hsrc).pin_memory()
     grp_e2e = DistRingGroup(src=x, starts=ring_starts(lens), lens=lens, acc=args.acc, lanes=args.e2e_lanes,
-                            protocol=args.protocol)
+                            protocol=args.protocol, options=plan_options(args))
     e2e_streams = [torch.cuda.Stream() for _ in range(args.e2e_lanes)]
 
     def e2e_step():
@@ -637,12 +792,15 @@ def run_multi(args, rank: int, world: int, local_rank: int):
             "ms_per_round": round(ms / (2 * (c - 1)), 5),
             "avg_kernel_ms": round(kernel_ms, 4),
             "ms_per_step_median": round(step_median, 4), "ms_per_step_min": round(step_min, 4),
-            "bus_gbps_per_gpu": round(bw, 3),
+            "bus_gbps_per_gpu": round(bw, 3), "bus_gbps_per_gpu_median": round(busbw(total, c, step_median * 1e-3), 3),
+            "timing": "each step starts after a rank-aligning NCCL all-reduce; per-step max over ranks, "
+                      "mean (ms_per_step) and median reported",
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" + (" (f64 fold)" if args.acc == "f64" else " (f32 fold)"),
             "data": "synthetic N(0,0.02) fp32 per cluster, torch Philox seeded",
             "config": {"workload": WORKLOAD_NAMES[args.workload], "clusters": c, "rings": len(lens),
                        "placement": "one cluster per GPU", "lanes": args.lanes, "protocol": grp.protocol,
+                       "plan_options": plan_options(args) or None,
                        "max_blocks": args.max_blocks or None,
                        "blend": (f"snapshot average + delayed-update blend, tau={args.tau}, "
                                  + ("in the cycle (push: fused per unit)" if in_cycle_blend else "separate launch")) if args.blend else None,
@@ -650,11 +808,18 @@ def run_multi(args, rank: int, world: int, local_rank: int):
                        "l2": l2_text},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_PEAK_GBS, 4),
+                         "achieved_median": round(alg_bytes / (kernel_median * 1e-3) / 1e9, 1),
                          "traffic": ncu_traffic(args.workload, c, world, args.acc) if grp.protocol == "push" else None,
-                         "pattern_ceiling": PATTERN_CEILING_GBS[grp.protocol],
-                         "frac_of_pattern_ceiling": round(achieved / PATTERN_CEILING_GBS[grp.protocol], 4),
-                         "basis": f"2(C-1)/C*S = {int(alg_bytes)} B per GPU per launch, each direction",
-                         "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)"},
+                         "measured_peer_copy": NVLINK_PEER_COPY_GBS,
+                         "frac_of_measured_peer_copy": round(achieved / NVLINK_PEER_COPY_GBS, 4),
+                         "pattern_ceiling": PATTERN_CEILING_GBS.get(grp.protocol),
+                         "frac_of_pattern_ceiling": round(achieved / PATTERN_CEILING_GBS[grp.protocol], 4)
+                         if grp.protocol in PATTERN_CEILING_GBS else None,
+                         "basis": f"2(C-1)/C*S = {int(alg_bytes)} B per GPU per launch, each direction; "
+                                  f"mean over steps of the per-step max over ranks",
+                         "peak_source": "NVLink 5 nominal 900 GB/s per direction per GPU (north_star, BASELINE.md); "
+                                        "secondary: 770 measured peer copy (B200_PROFILING.md), pattern ceiling "
+                                        "from ncu protocol overheads (profiles/r01/ncu_nvlink.md)"},
             "e2e": {"value": round(busbw(total, c, e2e_ms * 1e-3) * world, 3), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": world * total * 4, "d2h_bytes_per_step": world * total * 4,
@@ -710,6 +875,20 @@ def nccl_compare(lens, x, world: int, steps: int, flush=None):
     return NcclRings(x, lens).report(steps, flush)
 
 
+def spawn_ranks(n: int) -> int:
+    """``python bench.py --gpus N`` without a launcher: start the N ranks
+    (one process per GPU) with torch.distributed.run on 127.0.0.1 and pass
+    rank 0's JSON line through.  Returns the launcher's exit code."""
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -725,8 +904,19 @@ def main():
     ap.add_argument("--protocol", choices=["auto", "pull", "push"], default="auto")
     ap.add_argument("--clusters", type=int, default=0, help="N=1 only: co-resident cluster count (default 8)")
     ap.add_argument("--cpu-sample-params", type=int, default=8_000_000)
-    ap.add_argument("--ref-sample-params", type=int, default=2_000_000)
+    ap.add_argument("--ref-sample-params", type=int, default=0,
+                    help="--impl reference: time the port on this many params per cluster instead of the "
+                         "unmodified reference on the full workload (0 = full)")
+    ap.add_argument("--ref-budget-s", type=float, default=60.0,
+                    help="--impl reference: cap on the timed full-size cycles (seconds)")
+    ap.add_argument("--cpu-port-params", type=int, default=2_000_000,
+                    help="cpu_baseline: params per cluster of the port sample")
     ap.add_argument("--nccl", type=int, default=1)
+    ap.add_argument("--min-cb", type=int, default=0, help="N>1: force the member-count kernel bucket (8: the 8-GPU kernel)")
+    ap.add_argument("--push-items", type=int, default=0, help="N>1: push work items per resident block (0: default)")
+    ap.add_argument("--blend-lag", type=int, default=-1, help="N>1: fused-blend lag in groups of C items (-1: default)")
+    ap.add_argument("--e2e-seam", type=int, default=1, help="N=1: time apply_ring_mean through the reference's seam")
+    ap.add_argument("--e2e-seam-steps", type=int, default=3)
     ap.add_argument("--blend", type=int, default=0, help="config 4: snapshot average + delayed-update blend")
     ap.add_argument("--tau", type=int, default=4)
     ap.add_argument("--fused-blend", type=int, default=1,
@@ -750,6 +940,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, n_gpus, rank)
         return
+    if world <= 1 and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -137,6 +137,31 @@ int rv_plan_set_push_peers(rv_plan *plan, void *const *areas);
 
 int rv_plan_set_timeout(rv_plan *plan, double seconds);
 
+/* Kernel and layout options.  Kernel choice and the push layout depend only
+ * on the schedule, the placement and these calls -- never on the process
+ * environment.  Defaults are the measured best (tuning table). */
+#define RV_OPT_MIN_CB 1     /* member-count bucket floor (0): run the 8/16-member kernels with fewer members */
+#define RV_OPT_TMA 2        /* 1 (default): TMA kernel for co-resident plans with 16 B-congruent buffers; 0: register kernel */
+#define RV_OPT_PUSH_ITEMS 3 /* push: work items per resident block that size the units (default 2) */
+#define RV_OPT_PUSH_DYN 4   /* push: 1 (default) blocks take work items from a counter; 0: static grid stride */
+#define RV_OPT_BLEND_LAG 5  /* push fused blend: groups of C items between a fold and its blends (-1 = two resident grids) */
+#define RV_OPT_LAYOUT_SMS 6 /* push: SM count the unit layout assumes (0 = this device's); ranks must agree */
+int rv_plan_set_option(rv_plan *plan, int option, int64_t value);
+
+/* Build the device tables now (every position must be bound) instead of at
+ * the first cycle, and report the push / LL layout: out[0] vectors per unit,
+ * out[1] staging elements per writer slot, out[2] unit-flag slots per (lane,
+ * writer), out[3] push work items of lane 0 (all zero for the pull transport,
+ * whose tables are per rank; out[3] zero for LL).  Multi-process groups compare it across
+ * ranks (it must be identical for push / LL to be correct). */
+int rv_plan_prepare(rv_plan *plan);
+int rv_plan_layout(rv_plan *plan, int64_t *out4);
+
+/* Non-blocking failure probe: nonzero once a cycle of this plan hit its stall
+ * timeout (a host-mapped word the kernels write next to the device status).
+ * Reading it after an event that follows the cycle needs no device sync. */
+int rv_plan_failed(rv_plan *plan);
+
 /* Cap the blocks a cycle keeps resident (0 = whole device).  An NVLink-bound
  * cycle needs only part of the SMs; the rest stay free for training kernels
  * running concurrently on other streams. */
@@ -161,9 +186,20 @@ int rv_allreduce_mean(rv_plan *plan, void *const *streams, int n_streams);
 int rv_allreduce_mean_host(rv_plan *plan, const void *const *host_src, void *const *host_dst,
                            void *const *streams, int n_streams);
 
+/* The same for lanes [first_lane, first_lane + n_lanes) only, so a caller can
+ * fill lane l+1's host buffers while lane l is in flight (the numpy drop-in
+ * path pipelines its float64 copy-in this way).  Every lane must be run once
+ * per cycle; lanes are issued in increasing order. */
+int rv_allreduce_mean_host_lanes(rv_plan *plan, int first_lane, int n_lanes, const void *const *host_src,
+                                 void *const *host_dst, void *const *streams, int n_streams);
+
 /* Blocking: device-side status of the plan (RV_OK or RV_E_TIMEOUT), and a
  * description of the first stall "(ring=r, phase=..., member=m)". */
 int rv_plan_status(rv_plan *plan, char *diag, size_t diag_len);
+/* Clears the status and re-aligns the lane bookkeeping so this plan can run
+ * again.  After a cross-rank stall every rank of the group must reset (or
+ * rebuild its plan) before the next cycle; resetting one rank alone leaves
+ * the peers' barrier epochs behind. */
 int rv_plan_reset_status(rv_plan *plan);
 int rv_plan_destroy(rv_plan *plan);
 

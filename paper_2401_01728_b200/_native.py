@@ -31,6 +31,15 @@ RV_PROTO_PULL = 0
 RV_PROTO_PUSH = 1
 RV_PROTO_LL = 2
 
+RV_OPT_MIN_CB = 1
+RV_OPT_TMA = 2
+RV_OPT_PUSH_ITEMS = 3
+RV_OPT_PUSH_DYN = 4
+RV_OPT_BLEND_LAG = 5
+RV_OPT_LAYOUT_SMS = 6
+OPTIONS = {"min_cb": RV_OPT_MIN_CB, "tma": RV_OPT_TMA, "push_items": RV_OPT_PUSH_ITEMS,
+           "push_dyn": RV_OPT_PUSH_DYN, "blend_lag": RV_OPT_BLEND_LAG, "layout_sms": RV_OPT_LAYOUT_SMS}
+
 RV_MAX_CLUSTERS = 16
 RV_MAX_RANKS = 16
 
@@ -55,11 +64,17 @@ SIGNATURES = {
     "rv_plan_push_area": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, ctypes.POINTER(ctypes.c_size_t)]),
     "rv_plan_set_push_peers": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp]),
     "rv_plan_set_timeout": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double]),
+    "rv_plan_set_option": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64]),
+    "rv_plan_prepare": (ctypes.c_int, [ctypes.c_void_p]),
+    "rv_plan_layout": (ctypes.c_int, [ctypes.c_void_p, _c_i64_p]),
+    "rv_plan_failed": (ctypes.c_int, [ctypes.c_void_p]),
     "rv_plan_set_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rv_plan_set_max_blocks": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rv_plan_read_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
     "rv_allreduce_mean": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, ctypes.c_int]),
     "rv_allreduce_mean_host": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, _c_void_pp, _c_void_pp, ctypes.c_int]),
+    "rv_allreduce_mean_host_lanes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _c_void_pp, _c_void_pp,
+                                                    _c_void_pp, ctypes.c_int]),
     "rv_plan_status": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
     "rv_plan_reset_status": (ctypes.c_int, [ctypes.c_void_p]),
     "rv_plan_destroy": (ctypes.c_int, [ctypes.c_void_p]),

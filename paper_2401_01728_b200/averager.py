@@ -31,7 +31,7 @@ from __future__ import annotations
 
 from .blend import blend_
 from .dist import DistRingGroup
-from .errors import ConfigError
+from .errors import ConfigError, StallError
 
 
 class AsyncAverager:
@@ -55,7 +55,8 @@ class AsyncAverager:
         self.snap = torch.empty_like(live)
         # tau = 0: nothing lands on live during the cycle, so the means go
         # straight into live (the blend would write exactly the mean there)
-        self.mean = live if tau == 0 else torch.empty_like(live)
+        # (a mean buffer never holds garbage: it starts as the live values)
+        self.mean = live if tau == 0 else live.clone()
         self.kappa, self.tau = kappa, tau
         self.train_stream = train_stream or torch.cuda.current_stream(live.device)
         self.avg_stream = torch.cuda.Stream(device=live.device, priority=-1)
@@ -70,8 +71,20 @@ class AsyncAverager:
         self._graph = None
         self._use_graph = graph
 
+    def _raise_if_failed(self) -> None:
+        if not self.group.failed():
+            return
+        self._pending_at = None
+        try:
+            self.group.check()
+        except StallError as e:
+            raise StallError(f"averaging cycle {self.cycles} stalled; live parameters left unblended: {e}") from e
+        raise StallError(f"averaging cycle {self.cycles} stalled; live parameters left unblended")
+
     def _launch(self):
         import torch
+
+        self._raise_if_failed()
 
         # snapshot on the side stream, after everything training has issued;
         # before_update() keeps the next write to `live` behind the copy
@@ -99,6 +112,17 @@ class AsyncAverager:
 
     def _finish(self):
         self.before_update()
+        # a stalled cycle (a peer slower than the timeout) skipped its folds:
+        # its means must not reach the live parameters.  The failure word is
+        # host-mapped, so after the cycle's event it reads without a device
+        # sync (only the side stream is waited for; tau updates have run
+        # since the launch, so the cycle has normally long finished).  With
+        # tau = 0 the means land in live directly (a stalled cycle leaves
+        # some units averaged and the rest as they were, never garbage); the
+        # next launch reports it.
+        if self.tau > 0:
+            self._done.synchronize()
+            self._raise_if_failed()
         self.train_stream.wait_event(self._done)
         if self.tau > 0:
             blend_(self.live, self.snap, self.mean, self.train_stream)

@@ -127,7 +127,15 @@ struct rv_plan {
   int block_threads = kThreads;
   size_t smem_bytes = 0;
   int max_blocks = 0;  // 0 = whole device; else cap on resident blocks (SM budget)
-  int push_dyn = 1;    // push: work items from a counter (RAVNEST_B200_PUSH_DYN=0: static stride)
+  // rv_plan_set_option (RV_OPT_*)
+  int min_cb = 0;             // member-count bucket floor
+  int use_tma = 1;            // co-resident TMA kernel when eligible
+  int64_t push_items = 2;     // push: work items per resident block (sizes the units)
+  int push_dyn = 1;           // push: work items from a counter (else static grid stride)
+  int64_t blend_lag_opt = -1; // push fused blend: lag in groups of C items (-1: two resident grids)
+  int layout_sms = 0;         // push: SM count the unit layout assumes (0: this device's)
+  unsigned *fail_host = nullptr;  // host-mapped failure word (rv_plan_failed)
+  unsigned *fail_dev = nullptr;   // its device alias
   bool blend = false;        // live bound on the local positions: every cycle ends with the blend
   bool fused_blend = false;  // ... inside the push kernel (else blend launches after each lane)
   int64_t mflag_off = 0;     // push: mean-delivered flags after the scatter flags (u64 index)
@@ -250,10 +258,6 @@ int upload(rv_plan::Lane &lane, const std::vector<Seg> &segs, const std::vector<
 // lanes (launches / streams per cycle) a plan can hold beyond one per ring
 constexpr int kMaxLanes = 64;
 
-// push: target work items (scatter + fold units) per resident block; more
-// items shrink the tail when blocks finish unevenly, fewer amortise flags
-constexpr int64_t kPushItemsPerBlock = 2;
-
 int build_tables(rv_plan *p) {
   for (int i = 0; i < p->C; ++i)
     if (!p->bound[i]) return set_err(RV_E_ARG, "cluster position %d is not bound", i);
@@ -306,32 +310,28 @@ int build_tables(rv_plan *p) {
   }
   p->use_push = push;
   p->fused_blend = p->blend && push && p->proto == RV_PROTO_PUSH;  // co-resident TMA: set below
-  {
-    const char *de = getenv("RAVNEST_B200_PUSH_DYN");  // tuning
-    p->push_dyn = de ? atoi(de) != 0 : 1;
-  }
   const bool ll = ll_active(p);
   if (ll && p->dtype != RV_DTYPE_F32) return set_err(RV_E_CONFIG, "the LL transport carries fp32 parameters only");
   const int mode = p->dtype == RV_DTYPE_F64 ? kF64 : (p->acc == RV_ACC_NATIVE ? kF32Native : kF32Acc64);
   int U = 1;
   int64_t tile_vecs = 0;
   DeviceGuard g(p->device);
-  const char *tma_env = getenv("RAVNEST_B200_TMA");
-  const bool tma = vec && p->n_ranks == 1 && !(tma_env && tma_env[0] == '0');
+  const bool tma = vec && p->n_ranks == 1 && p->use_tma;
+  const int cb = bucket_c(p->C, p->min_cb);
   if (ll) {
-    p->kernel = pick_ll_kernel(mode, p->C);
+    p->kernel = pick_ll_kernel(mode, cb);
     p->block_threads = kThreads;
     p->smem_bytes = 0;
     tile_vecs = kLLUnit;
   } else if (tma) {
     int tv = 0;
     p->fused_blend = p->blend;
-    p->kernel = pick_tma_kernel(mode, p->C, p->blend, &tv, &p->smem_bytes);
+    p->kernel = pick_tma_kernel(mode, cb, p->blend, &tv, &p->smem_bytes);
     p->block_threads = kTmaConsumers + 32;
     RV_CUDA(cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem_bytes));
     tile_vecs = tv;
   } else {
-    p->kernel = pick_kernel(mode, p->C, vec, push, &U);
+    p->kernel = pick_kernel(mode, cb, vec, push, &U);
     p->block_threads = kThreads;
     p->smem_bytes = 0;
     tile_vecs = (int64_t)kThreads * U;
@@ -353,9 +353,10 @@ int build_tables(rv_plan *p) {
       }
       owner_elems = std::max(owner_elems, e);
     }
-    const char *ie = getenv("RAVNEST_B200_PUSH_ITEMS");  // work items per resident block (tuning)
-    const int64_t per_block = ie ? std::max(1, atoi(ie)) : kPushItemsPerBlock;
-    const int64_t items = std::max<int64_t>(1, per_block * p->sm_count * p->occ);
+    // target work items (scatter + fold units) per resident block: more
+    // shrink the tail when blocks finish unevenly, fewer amortise the flags
+    const int64_t sms = p->layout_sms > 0 ? p->layout_sms : p->sm_count;
+    const int64_t items = std::max<int64_t>(1, p->push_items * sms * p->occ);
     const int64_t want = (owner_elems / N * (p->C - 1) + items - 1) / items;
     const int64_t lo = kMinUnitBytes / (N * es), hi = kUnitBytes / (N * es);
     unit_vecs = std::min(hi, std::max(lo, (want + kThreads - 1) / kThreads * kThreads));
@@ -449,11 +450,11 @@ int build_tables(rv_plan *p) {
         lane.umax_all = std::max(lane.umax_all, lane.ounits[q]);
       }
       // fused blend: a unit's blends trail its fold by about two resident
-      // grids of items (RAVNEST_B200_BLEND_LAG: groups of C items, tuning;
-      // GPT-2 at 4 GPUs, 1 / 2 / 4 / 8 / 16 grids: 3.53 / 3.22 / 3.28 /
-      // 3.47 / 3.77 ms per cycle + blend)
-      lane.blend_lag = (2 * (int64_t)p->sm_count * p->occ + p->C - 1) / p->C;
-      if (const char *be = getenv("RAVNEST_B200_BLEND_LAG")) lane.blend_lag = std::max(0, atoi(be));
+      // grids of items (RV_OPT_BLEND_LAG: groups of C items; GPT-2 at 4
+      // GPUs, 1 / 2 / 4 / 8 / 16 grids: 3.53 / 3.22 / 3.28 / 3.47 / 3.77 ms
+      // per cycle + blend).  Every rank must use the same lag.
+      lane.blend_lag = p->blend_lag_opt >= 0 ? p->blend_lag_opt
+                                             : (2 * (int64_t)p->sm_count * p->occ + p->C - 1) / p->C;
       lane.n_tiles = ll ? (int64_t)(p->C - 1) * lane.scatter_umax * 2 + lane.ounits[p->rank]
                         : (int64_t)(p->fused_blend ? 2 * p->C - 1 : p->C) * lane.umax_all;
       lane.nseg = (int)segs.size();
@@ -475,13 +476,26 @@ int build_tables(rv_plan *p) {
   // another on this device while both wait on peers)
   int64_t capacity = (int64_t)p->sm_count * p->occ;
   if (p->max_blocks > 0) capacity = std::min<int64_t>(capacity, p->max_blocks);
+  std::vector<int64_t> share(p->n_lanes);
+  int64_t granted = 0;
   for (int l = 0; l < p->n_lanes; ++l) {
-    rv_plan::Lane &lane = p->lanes[l];
-    int64_t share = all_elems > 0 ? capacity * lane.elems / all_elems : 0;
-    if (p->n_lanes == 1) share = capacity;
-    share = std::max<int64_t>(1, std::min<int64_t>(share, std::max<int64_t>(1, lane.n_tiles)));
-    lane.grid = (int)share;
+    const rv_plan::Lane &lane = p->lanes[l];
+    int64_t sh = all_elems > 0 ? capacity * lane.elems / all_elems : 0;
+    if (p->n_lanes == 1) sh = capacity;
+    share[l] = std::max<int64_t>(1, std::min<int64_t>(sh, std::max<int64_t>(1, lane.n_tiles)));
+    granted += share[l];
   }
+  // the one-block floor of small lanes must not push the sum past the
+  // budget (lanes spin on peers: every block of every lane must be resident)
+  while (granted > capacity) {
+    int big = 0;
+    for (int l = 1; l < p->n_lanes; ++l)
+      if (share[l] > share[big]) big = l;
+    if (share[big] <= 1) break;  // more lanes than blocks: cannot fit, keep one each
+    --share[big];
+    --granted;
+  }
+  for (int l = 0; l < p->n_lanes; ++l) p->lanes[l].grid = (int)share[l];
   p->dirty = false;
   return RV_OK;
 }
@@ -501,6 +515,7 @@ int launch_lane(rv_plan *p, int l, cudaStream_t st) {
   cp.my_flags = p->flags;
   cp.state = p->states + l;
   cp.status = p->status;
+  cp.fail_host = p->fail_dev;
   if (p->trace) {
     cp.trace = p->trace + 4 * l;
     RV_CUDA(cudaMemsetAsync(cp.trace, 0xff, sizeof(unsigned long long), st));
@@ -599,10 +614,6 @@ int rv_plan_create(rv_plan **out, int device, int n_clusters, int n_rings, const
   p->live.assign(n_clusters, nullptr);
   p->bound.assign(n_clusters, 0);
   p->peer_flags.assign(RV_MAX_RANKS, nullptr);
-  if (const char *t = getenv("RAVNEST_B200_TIMEOUT_S")) {
-    const double s = atof(t);
-    if (s > 0) p->timeout_ns = (unsigned long long)(s * 1e9);
-  }
   {
     DeviceGuard g(device);
     cudaError_t e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device);
@@ -614,6 +625,11 @@ int rv_plan_create(rv_plan **out, int device, int n_clusters, int n_rings, const
     if (e == cudaSuccess) e = cudaMemset(p->states, 0, sizeof(LaneState) * lanes_cap);
     if (e == cudaSuccess) e = cudaMalloc(&p->status, 4 * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(p->status, 0, 4 * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaHostAlloc(&p->fail_host, sizeof(unsigned), cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess) {
+      *(volatile unsigned *)p->fail_host = 0u;
+      e = cudaHostGetDevicePointer(&p->fail_dev, p->fail_host, 0);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       rv_plan_destroy(p);
@@ -789,6 +805,57 @@ int rv_plan_set_max_blocks(rv_plan *p, int max_blocks) {
   return RV_OK;
 }
 
+int rv_plan_set_option(rv_plan *p, int option, int64_t value) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  switch (option) {
+    case RV_OPT_MIN_CB:
+      if (value < 0 || value > RV_MAX_CLUSTERS) return set_err(RV_E_ARG, "min_cb must be in [0, %d]", RV_MAX_CLUSTERS);
+      p->min_cb = (int)value;
+      break;
+    case RV_OPT_TMA: p->use_tma = value != 0; break;
+    case RV_OPT_PUSH_ITEMS:
+      if (value < 1 || value > 1024) return set_err(RV_E_ARG, "push items per block must be in [1, 1024]");
+      p->push_items = value;
+      break;
+    case RV_OPT_PUSH_DYN: p->push_dyn = value != 0; break;
+    case RV_OPT_BLEND_LAG:
+      if (value < -1) return set_err(RV_E_ARG, "blend lag must be >= -1");
+      p->blend_lag_opt = value;
+      break;
+    case RV_OPT_LAYOUT_SMS:
+      if (value < 0 || value > 4096) return set_err(RV_E_ARG, "layout SM count must be in [0, 4096]");
+      p->layout_sms = (int)value;
+      break;
+    default: return set_err(RV_E_ARG, "unknown option %d", option);
+  }
+  p->dirty = true;
+  return RV_OK;
+}
+
+int rv_plan_prepare(rv_plan *p) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  DeviceGuard g(p->device);
+  if (p->dirty || p->ptrs_dirty) return build_tables(p);
+  return RV_OK;
+}
+
+int rv_plan_layout(rv_plan *p, int64_t *out4) {
+  if (!p || !out4) return set_err(RV_E_ARG, "NULL argument");
+  if (p->dirty || p->lanes.empty()) return set_err(RV_E_ARG, "plan tables not built (call rv_plan_prepare)");
+  out4[0] = p->use_push ? p->lanes[0].unit_vecs : 0;
+  out4[1] = p->use_push ? p->stride_bound : 0;
+  out4[2] = p->use_push ? p->units_max : 0;
+  // work items of the push work order (every rank walks the same list); the
+  // pull and LL tables hold this rank's own items only
+  out4[3] = p->use_push && !ll_active(p) ? p->lanes[0].n_tiles : 0;
+  return RV_OK;
+}
+
+int rv_plan_failed(rv_plan *p) {
+  if (!p || !p->fail_host) return 0;
+  return (int)*(volatile unsigned *)p->fail_host;
+}
+
 int rv_plan_set_timeout(rv_plan *p, double seconds) {
   if (!p || !(seconds > 0)) return set_err(RV_E_ARG, "bad timeout");
   p->timeout_ns = (unsigned long long)(seconds * 1e9);
@@ -822,14 +889,16 @@ int rv_allreduce_mean(rv_plan *p, void *const *streams, int n_streams) {
   return RV_OK;
 }
 
-int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const *host_dst,
-                           void *const *streams, int n_streams) {
+int rv_allreduce_mean_host_lanes(rv_plan *p, int first_lane, int n_lanes, const void *const *host_src,
+                                 void *const *host_dst, void *const *streams, int n_streams) {
   if (!p || !host_src || !host_dst) return set_err(RV_E_ARG, "NULL argument");
   DeviceGuard g(p->device);
   if (p->dirty || p->ptrs_dirty) {
     int rc = build_tables(p);
     if (rc) return rc;
   }
+  if (first_lane < 0 || n_lanes < 0 || first_lane + n_lanes > p->n_lanes)
+    return set_err(RV_E_ARG, "lanes [%d, %d) outside the plan's %d", first_lane, first_lane + n_lanes, p->n_lanes);
   if (p->blend) return set_err(RV_E_ARG, "the host-buffer path does not blend (unbind the live buffers)");
   const int es = elem_size(p->dtype);
   // host->device copies run lane after lane (lane l's kernel starts as soon
@@ -840,7 +909,7 @@ int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const 
     RV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     p->h2d_done.push_back(e);
   }
-  for (int l = 0; l < p->n_lanes; ++l) {
+  for (int l = first_lane; l < first_lane + n_lanes; ++l) {
     cudaStream_t st = (streams && n_streams > 0) ? (cudaStream_t)streams[l % n_streams] : (cudaStream_t)0;
     const rv_plan::Lane &lane = p->lanes[l];
     const size_t off = (size_t)lane.lo * es, bytes = (size_t)(lane.hi - lane.lo) * es;
@@ -860,6 +929,12 @@ int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const 
     }
   }
   return RV_OK;
+}
+
+int rv_allreduce_mean_host(rv_plan *p, const void *const *host_src, void *const *host_dst,
+                           void *const *streams, int n_streams) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  return rv_allreduce_mean_host_lanes(p, 0, p->n_lanes, host_src, host_dst, streams, n_streams);
 }
 
 int rv_plan_status(rv_plan *p, char *diag, size_t diag_len) {
@@ -886,8 +961,21 @@ int rv_plan_status(rv_plan *p, char *diag, size_t diag_len) {
 int rv_plan_reset_status(rv_plan *p) {
   if (!p) return set_err(RV_E_ARG, "plan is NULL");
   DeviceGuard g(p->device);
-  RV_CUDA(cudaMemset(p->status, 0, 4 * sizeof(unsigned)));
   RV_CUDA(cudaDeviceSynchronize());
+  RV_CUDA(cudaMemset(p->status, 0, 4 * sizeof(unsigned)));
+  // a cycle that ran with the status set advanced its epoch without posting
+  // arrive flags: re-align `signaled` so the next cycle posts them again
+  const int lanes_cap = std::max(kMaxLanes, p->R);
+  std::vector<LaneState> st(lanes_cap);
+  RV_CUDA(cudaMemcpy(st.data(), p->states, sizeof(LaneState) * lanes_cap, cudaMemcpyDeviceToHost));
+  for (auto &s : st) {
+    s.signaled = s.epoch;
+    s.done = 0u;
+    s.grab = 0u;
+  }
+  RV_CUDA(cudaMemcpy(p->states, st.data(), sizeof(LaneState) * lanes_cap, cudaMemcpyHostToDevice));
+  RV_CUDA(cudaDeviceSynchronize());
+  *(volatile unsigned *)p->fail_host = 0u;
   return RV_OK;
 }
 
@@ -902,6 +990,7 @@ int rv_plan_destroy(rv_plan *p) {
     if (p->flags) cudaFree(p->flags);
     if (p->states) cudaFree(p->states);
     if (p->status) cudaFree(p->status);
+    if (p->fail_host) cudaFreeHost(p->fail_host);
   }
   delete p;
   return RV_OK;

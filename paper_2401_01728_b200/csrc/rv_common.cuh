@@ -75,6 +75,7 @@ struct CycleParams {
   unsigned long long *my_flags;
   LaneState *state;
   unsigned int *status;        // [0] code, [1] diag
+  unsigned int *fail_host;     // host-mapped failure word (rv_plan_failed)
   unsigned long long *trace;   // optional: [start, ready, work done, departed] (globaltimer ns)
   int64_t n_tiles;             // pull
   int64_t stride;              // push: staging elements per writer slot
@@ -120,6 +121,15 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
+// Record a stall: the first failing thread sets the device status and its
+// diagnostic, and raises the host-visible failure word.
+__device__ __forceinline__ void fail(const CycleParams &p, unsigned diag) {
+  if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u) {
+    p.status[1] = diag;
+    if (p.fail_host) *(volatile unsigned *)p.fail_host = 1u;
+  }
+}
+
 // Spin until *f >= e.  Returns false on timeout (status set, diag recorded)
 // or when another block already failed.
 __device__ bool wait_flag(const CycleParams &p, const unsigned long long *f, unsigned long long e,
@@ -129,7 +139,7 @@ __device__ bool wait_flag(const CycleParams &p, const unsigned long long *f, uns
     if ((++spins & 255u) == 0) {
       if (*(volatile unsigned *)p.status != 0) return false;
       if (globaltimer() - t0 > p.timeout_ns) {
-        if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u) p.status[1] = diag;
+        fail(p, diag);
         return false;
       }
     }

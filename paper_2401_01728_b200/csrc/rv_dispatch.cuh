@@ -9,15 +9,12 @@
 
 using KernelFn = void (*)(CycleParams);
 
-// RAVNEST_B200_MIN_CB (tests only): instantiate at least this member-count
-// bucket, so the CB = 8 / 16 kernels of 8- and 16-GPU jobs run, with fewer
-// members, on the GPUs a test box has.  Results are unchanged: every kernel
-// loops over the runtime C and uses CB only as a register-array bound.
-int bucket_c(int c) {
-  const char *e = getenv("RAVNEST_B200_MIN_CB");
-  const int floor = e ? atoi(e) : 0;
-  return floor > c ? std::min(floor, RV_MAX_CLUSTERS) : c;
-}
+// Member-count bucket: the smallest instantiated CB >= c, raised to
+// `min_cb` (RV_OPT_MIN_CB) so the CB = 8 / 16 kernels of 8- and 16-GPU jobs
+// run, with fewer members, on the GPUs a test box has.  Results are
+// unchanged: every kernel loops over the runtime C and uses CB only as a
+// register-array bound.
+int bucket_c(int c, int min_cb) { return min_cb > c ? std::min(min_cb, RV_MAX_CLUSTERS) : c; }
 
 enum Mode { kF32Acc64 = 0, kF32Native = 1, kF64 = 2 };
 
@@ -53,25 +50,12 @@ KernelFn pick_cb(int c, bool push, int *u_out) {
   return ring_cycle_kernel<T, Acc, 16, VB, 1>;
 }
 
-// Tuning variants of the f32 / f64-fold vector pull kernel (RAVNEST_B200_VARIANT,
-// experiments only): 1 = half the vectors per thread, >= 3 blocks/SM;
-// 2 = half, >= 4 blocks/SM; 3 = same vectors, no register cap (1 block/SM).
-template <int CB, int U>
-KernelFn pick_variant(int v, int *u_out) {
-  constexpr int H = U > 1 ? U / 2 : 1;
-  switch (v) {
-    case 1: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 3>;
-    case 2: *u_out = H; return ring_cycle_kernel<float, double, CB, 16, H, 4>;
-    case 3: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 1>;
-    default: *u_out = U; return ring_cycle_kernel<float, double, CB, 16, U, 2>;
-  }
-}
-
 // Co-resident TMA kernel: 64 KB of member data per pipeline stage
 // (CB * TV * 16 bytes), 2 stages -> 136-192 KB of shared memory, one block
 // per SM.  Measured on BERT / ResNet-50 C=8 against 3 x 32 KB with two
 // blocks per SM (0.895 / 0.878 of measured HBM): 0.905-0.933 / 0.919-0.922;
-// 2 x 32/40/48/80/96 KB and 3 x 64 KB were slower (RAVNEST_B200_TMA_VARIANT).
+// 2 x 32/40/48/80/96 KB, 3 x 64 KB, 6 x 32 KB, 8 x 16 KB and L2 evict-first
+// hints were slower (round-1 experiment builds, DESIGN.md tuning table).
 constexpr int kTmaStages = 2;
 constexpr int kTmaStageBytes = 64 * 1024;
 
@@ -82,75 +66,39 @@ KernelFn pick_tma(int c, int *tv_out) {
   constexpr int K = BL ? 2 : 1;
   if (c <= 2) {
     *tv_out = STAGE_BYTES / (K * 2 * 16);
-    return ring_tma_kernel<T, Acc, 2, STAGE_BYTES / (K * 2 * 16), STAGES, false, BL>;
+    return ring_tma_kernel<T, Acc, 2, STAGE_BYTES / (K * 2 * 16), STAGES, BL>;
   }
   if (c <= 4) {
     *tv_out = STAGE_BYTES / (K * 4 * 16);
-    return ring_tma_kernel<T, Acc, 4, STAGE_BYTES / (K * 4 * 16), STAGES, false, BL>;
+    return ring_tma_kernel<T, Acc, 4, STAGE_BYTES / (K * 4 * 16), STAGES, BL>;
   }
   if (c <= 8) {
     *tv_out = STAGE_BYTES / (K * 8 * 16);
-    return ring_tma_kernel<T, Acc, 8, STAGE_BYTES / (K * 8 * 16), STAGES, false, BL>;
+    return ring_tma_kernel<T, Acc, 8, STAGE_BYTES / (K * 8 * 16), STAGES, BL>;
   }
   *tv_out = STAGE_BYTES / (K * 16 * 16);
-  return ring_tma_kernel<T, Acc, 16, STAGE_BYTES / (K * 16 * 16), STAGES, false, BL>;
+  return ring_tma_kernel<T, Acc, 16, STAGE_BYTES / (K * 16 * 16), STAGES, BL>;
 }
 
 KernelFn pick_tma_kernel(int mode, int c, bool blend, int *tv_out, size_t *smem_out) {
-  c = bucket_c(c);
-  if (blend) {
-    KernelFn k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes, true>(c, tv_out)
-               : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes, true>(c, tv_out)
-                                    : pick_tma<double, double, kTmaStages, kTmaStageBytes, true>(c, tv_out);
-    const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
-    *smem_out = (size_t)kTmaStages * 2 * cb * (*tv_out) * 16 + 2 * (size_t)(cb + 1) * (*tv_out) * 16;
-    return k;
-  }
-  // RAVNEST_B200_TMA_VARIANT (experiments): 1 = 6 stages, 2 = 4 stages (one
-  // block per SM), 3 = 8 stages of 16 KB, 4 = L2 evict-first hints,
-  // 5 = 3 x 64 KB (one block per SM), 6 = 3 x 32 KB (two blocks per SM;
-  // the first default), 7 = 2 x 48 KB,
-  // 8 = 2 x 96 KB, 9 = 2 x 80 KB, 10 = 2 x 32 KB, 11 = 2 x 40 KB
-  const char *ve = getenv("RAVNEST_B200_TMA_VARIANT");
-  const int v = ve ? atoi(ve) : 0;
-  int stages = kTmaStages;
   KernelFn k;
-  if (v > 0 && mode == kF32Acc64) {
-    if (v == 1) { stages = 6; k = pick_tma<float, double, 6, 32 * 1024>(c, tv_out); }
-    else if (v == 2) { stages = 4; k = pick_tma<float, double, 4, 32 * 1024>(c, tv_out); }
-    else if (v == 4) {
-      k = c <= 8 ? (KernelFn)ring_tma_kernel<float, double, 8, kTmaStageBytes / (8 * 16), kTmaStages, true>
-                 : pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out);
-      *tv_out = c <= 8 ? kTmaStageBytes / (8 * 16) : *tv_out;
-    }
-    else if (v == 5) { stages = 3; k = pick_tma<float, double, 3, 64 * 1024>(c, tv_out); }
-    else if (v == 6) { stages = 3; k = pick_tma<float, double, 3, 32 * 1024>(c, tv_out); }
-    else if (v == 7) { stages = 2; k = pick_tma<float, double, 2, 48 * 1024>(c, tv_out); }
-    else if (v == 8) { stages = 2; k = pick_tma<float, double, 2, 96 * 1024>(c, tv_out); }
-    else if (v == 9) { stages = 2; k = pick_tma<float, double, 2, 80 * 1024>(c, tv_out); }
-    else if (v == 10) { stages = 2; k = pick_tma<float, double, 2, 32 * 1024>(c, tv_out); }
-    else if (v == 11) { stages = 2; k = pick_tma<float, double, 2, 40 * 1024>(c, tv_out); }
-    else { stages = 8; k = pick_tma<float, double, 8, 16 * 1024>(c, tv_out); }
-  } else {
+  if (blend)
+    k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes, true>(c, tv_out)
+      : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes, true>(c, tv_out)
+                           : pick_tma<double, double, kTmaStages, kTmaStageBytes, true>(c, tv_out);
+  else
     k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out)
       : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes>(c, tv_out)
                            : pick_tma<double, double, kTmaStages, kTmaStageBytes>(c, tv_out);
-  }
   const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
-  *smem_out = (size_t)stages * cb * (*tv_out) * 16 + 3 * (size_t)(*tv_out) * 16;  // 3 output buffers
+  // input stages, then the output buffers: 3 mean tiles, or (blend) 2 x
+  // (mean + C live tiles) -- must match ring_tma_kernel's NOB / OUTS
+  *smem_out = blend ? (size_t)kTmaStages * 2 * cb * (*tv_out) * 16 + 2 * (size_t)(cb + 1) * (*tv_out) * 16
+                    : (size_t)kTmaStages * cb * (*tv_out) * 16 + 3 * (size_t)(*tv_out) * 16;
   return k;
 }
 
 KernelFn pick_kernel(int mode, int c, bool vec, bool push, int *u_out) {
-  c = bucket_c(c);
-  const char *ve = getenv("RAVNEST_B200_VARIANT");
-  const int variant = ve ? atoi(ve) : 0;
-  if (variant > 0 && mode == kF32Acc64 && vec && !push) {
-    if (c <= 2) return pick_variant<2, 8>(variant, u_out);
-    if (c <= 4) return pick_variant<4, 4>(variant, u_out);
-    if (c <= 8) return pick_variant<8, 2>(variant, u_out);
-    return pick_variant<16, 1>(variant, u_out);
-  }
   switch (mode) {
     case kF32Acc64: return vec ? pick_cb<float, double, 16>(c, push, u_out) : pick_cb<float, double, 4>(c, push, u_out);
     case kF32Native: return vec ? pick_cb<float, float, 16>(c, push, u_out) : pick_cb<float, float, 4>(c, push, u_out);
@@ -168,6 +116,5 @@ KernelFn pick_ll(int c) {
 }
 
 KernelFn pick_ll_kernel(int mode, int c) {
-  c = bucket_c(c);
   return mode == kF32Native ? pick_ll<float>(c) : pick_ll<double>(c);
 }

@@ -9,10 +9,43 @@
 // HBM or NVLink peer loads) and pushes the mean into every member.  Arrive
 // barrier first (peers' inputs final), depart barrier last.
 
+// Segment of tile t for a thread whose tiles increase (t = blockIdx.x +
+// i * gridDim.x): one binary search over tile_prefix for the first tile, then
+// a forward walk, reloading the chunk record only when the segment changes
+// (a binary search per tile cost 1% of HBM bandwidth on the TMA kernel,
+// profiles/r01/ab_tma_segwalk_n1.txt).
+struct SegWalk {
+  int a = -1;
+  int64_t next = 0, base = 0;  // tile_prefix[a + 1], tile_prefix[a]
+  Seg cur;
+  __device__ __forceinline__ const Seg &at(const CycleParams &p, int64_t t, int64_t *local) {
+    if (a < 0) {
+      int lo = 0, hi = p.nseg - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(p.tile_prefix + mid) <= t) lo = mid; else hi = mid - 1;
+      }
+      a = lo;
+      base = __ldg(p.tile_prefix + a);
+      next = __ldg(p.tile_prefix + a + 1);
+      cur = p.segs[a];
+    } else if (t >= next) {
+      int b = a + 1;
+      while (__ldg(p.tile_prefix + b + 1) <= t) ++b;
+      a = b;
+      base = __ldg(p.tile_prefix + a);
+      next = __ldg(p.tile_prefix + a + 1);
+      cur = p.segs[a];
+    }
+    *local = t - base;
+    return cur;
+  }
+};
+
 // Two 256-thread blocks per SM (<= 128 registers): measured 1.18 ms vs
 // 1.47 ms at one block per SM on the co-resident BERT cycle.
-template <typename T, typename Acc, int CB, int VB, int U, int MINB = 2>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <typename T, typename Acc, int CB, int VB, int U>
+__global__ void __launch_bounds__(kThreads, 2)
 ring_cycle_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = VB / sizeof(T);
   __shared__ int s_go;
@@ -42,14 +75,10 @@ ring_cycle_kernel(const __grid_constant__ CycleParams p) {
 
   if (s_go) {
     const int64_t tile_vecs = (int64_t)kThreads * U;
+    SegWalk walk;
     for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-      int a = 0, b = p.nseg - 1;
-      while (a < b) {
-        const int mid = (a + b + 1) >> 1;
-        if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
-      }
-      const Seg s = p.segs[a];
-      const int64_t local_tile = t - __ldg(p.tile_prefix + a);
+      int64_t local_tile;
+      const Seg s = walk.at(p, t, &local_tile);
       const int64_t nvec = (s.body_hi - s.body_lo) / N;
       const int64_t jbeg = local_tile * tile_vecs;
       fold_pass<T, Acc, CB, VB, U, false>(p, s, jbeg + threadIdx.x, min(nvec, jbeg + tile_vecs));
@@ -302,7 +331,7 @@ __device__ __forceinline__ bool ll_load(const CycleParams &p, const unsigned *ad
       if (t0 == 0) t0 = globaltimer();
       if (*(volatile unsigned *)p.status != 0) return false;
       if (globaltimer() - t0 > p.timeout_ns) {
-        if (atomicCAS(p.status, 0u, kStatusTimeout) == 0u) p.status[1] = diag;
+        fail(p, diag);
         return false;
       }
     }
@@ -466,28 +495,6 @@ __device__ __forceinline__ void bulk_load(void *smem, const void *gmem, unsigned
                : "memory");
 }
 
-__device__ __forceinline__ void bulk_load_hint(void *smem, const void *gmem, unsigned bytes, unsigned long long *bar,
-                                               unsigned long long policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_addr(smem)),
-      "l"(gmem), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_store_hint(void *gmem, const void *smem, unsigned bytes,
-                                                unsigned long long policy) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem),
-               "r"(smem_addr(smem)), "r"(bytes), "l"(policy)
-               : "memory");
-}
-
-__device__ __forceinline__ unsigned long long evict_first_policy() {
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
 __device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)),
                "r"(bytes)
@@ -497,7 +504,7 @@ __device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigne
 // BL (fused delayed-update blend): each stage also carries every member's
 // live tile; the consumers write the mean tile and C blended live tiles,
 // which go out by bulk store to dst and live.
-template <typename T, typename Acc, int CB, int TV, int STAGES, bool HINT = false, bool BL = false>
+template <typename T, typename Acc, int CB, int TV, int STAGES, bool BL = false>
 __global__ void __launch_bounds__(kTmaConsumers + 32, 2)
 ring_tma_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = 16 / sizeof(T);
@@ -521,35 +528,10 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
   }
   __syncthreads();
 
-  // the tiles this block owns: t = blockIdx.x + i * gridDim.x, increasing,
-  // so each thread walks the segment table forward from its last segment
-  // (one binary search for the first tile) and reloads the chunk record only
-  // when the segment changes
-  int seg_a = -1;
-  int64_t seg_next = 0, seg_base = 0;  // tile_prefix[seg_a + 1], tile_prefix[seg_a]
-  Seg seg_cur;
-  auto seg_of = [&](int64_t t, int64_t *local) -> const Seg & {
-    if (seg_a < 0) {
-      int a = 0, b = p.nseg - 1;
-      while (a < b) {
-        const int mid = (a + b + 1) >> 1;
-        if (__ldg(p.tile_prefix + mid) <= t) a = mid; else b = mid - 1;
-      }
-      seg_a = a;
-      seg_base = __ldg(p.tile_prefix + a);
-      seg_next = __ldg(p.tile_prefix + a + 1);
-      seg_cur = p.segs[a];
-    } else if (t >= seg_next) {
-      int a = seg_a + 1;
-      while (__ldg(p.tile_prefix + a + 1) <= t) ++a;
-      seg_a = a;
-      seg_base = __ldg(p.tile_prefix + a);
-      seg_next = __ldg(p.tile_prefix + a + 1);
-      seg_cur = p.segs[a];
-    }
-    *local = t - seg_base;
-    return seg_cur;
-  };
+  // the tiles this block owns increase (t = blockIdx.x + i * gridDim.x), so
+  // each thread walks the segment table forward (SegWalk)
+  SegWalk walk;
+  auto seg_of = [&](int64_t t, int64_t *local) -> const Seg & { return walk.at(p, t, local); };
 
   if (tid < 32) {
     if (tid == 0) {  // producer
@@ -568,13 +550,8 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
           for (int q = 0; q < C; ++q) {
             int m = s.k + q;
             if (m >= C) m -= C;
-            if constexpr (HINT)
-              bulk_load_hint(in + ((size_t)stage * SLOTS + q) * TV,
-                             static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N, (unsigned)(cnt * 16),
-                             &full[stage], evict_first_policy());
-            else
-              bulk_load(in + ((size_t)stage * SLOTS + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
-                        (unsigned)(cnt * 16), &full[stage]);
+            bulk_load(in + ((size_t)stage * SLOTS + q) * TV, static_cast<const T *>(p.src[m]) + s.body_lo + j0 * N,
+                      (unsigned)(cnt * 16), &full[stage]);
             if constexpr (BL)
               bulk_load(in + ((size_t)stage * SLOTS + CB + q) * TV,
                         static_cast<const T *>(p.live[m]) + s.body_lo + j0 * N, (unsigned)(cnt * 16), &full[stage]);
@@ -641,11 +618,7 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
       if (cnt > 0) {
         const uint4 *mean_tile = out + (size_t)ob * OUTS * TV;
         for (int q = 0; q < C; ++q)
-          if constexpr (HINT)
-            bulk_store_hint(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, mean_tile, (unsigned)(cnt * 16),
-                            evict_first_policy());
-          else
-            bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, mean_tile, (unsigned)(cnt * 16));
+          bulk_store(static_cast<T *>(p.dst[q]) + s.body_lo + j0 * N, mean_tile, (unsigned)(cnt * 16));
         if constexpr (BL)
           for (int q = 0; q < C; ++q) {
             int m = s.k + q;

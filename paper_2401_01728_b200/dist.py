@@ -92,7 +92,7 @@ class DistRingGroup:
     def __init__(self, schedule=None, src=None, dst=None, *, starts: Sequence[int] | None = None,
                  lens: Sequence[int] | None = None, cluster_id: int | None = None, acc: str = "f64",
                  lanes: int = 1, group=None, timeout_s: float | None = None, protocol: str = "auto",
-                 max_blocks: int = 0, live=None):
+                 max_blocks: int = 0, live=None, options: dict | None = None):
         import torch.distributed as dist
 
         if src is None:
@@ -129,6 +129,7 @@ class DistRingGroup:
         cid = self.rank if cluster_id is None else int(cluster_id)
 
         self.plan = DevicePlan(self.device, self.world, starts, lens, total, _dtype_code(src.dtype), acc)
+        self.plan.set_options(options)
         if lanes != 1:
             self.plan.set_lanes(lanes)
         if timeout_s is not None:
@@ -176,23 +177,61 @@ class DistRingGroup:
         self.live = None
         if live is not None:
             self.bind_live(live)
+        else:
+            self._agree()
         dist.barrier(group=group)
+
+    def _agree(self) -> None:
+        """Build the tables and check every rank derived the same layout:
+        push and LL writers compute the owners' staging addresses and unit
+        flags locally, so a rank with another SM count or option set would
+        corrupt the means or hang.  Raises ConfigError on a mismatch."""
+        import torch.distributed as dist
+
+        self.plan.prepare()
+        mine = self.plan.layout()
+        everyone: list = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=self.group)
+        if any(e != mine for e in everyone):
+            raise ConfigError(f"ranks derived different cycle layouts (unit vectors, stride, unit slots, "
+                              f"work items): {everyone}; use the same options on every rank "
+                              f"(e.g. layout_sms for GPUs with different SM counts)")
 
     def bind_live(self, live) -> None:
         """Fuse the delayed-update blend into every cycle: ``live`` (this
         rank's live parameters) ends each cycle as mean + (live - src), the
         snapshot ``src`` having been averaged into ``dst``.  ``None`` unbinds.
-        Local to this rank; every rank should bind or none (the push kernel
-        then blends unit by unit as the means land)."""
+        Collective: every rank must bind (or unbind) together -- the push
+        kernel then blends unit by unit as the means land and skips the depart
+        barrier, so a rank without the blend would wait for flags nobody
+        raises.  Raises ConfigError when the ranks disagree."""
+        import torch.distributed as dist
+
+        err = None
         if live is not None:
             if not live.is_cuda or not live.is_contiguous() or live.numel() != self.total:
-                raise LayoutError("live must be a contiguous CUDA tensor shaped like the parameter vector")
-            if live.dtype != self.src.dtype or live.device.index != self.device:
-                raise LayoutError("live must match the parameter buffer's dtype and device")
-            if self.dst.data_ptr() == self.src.data_ptr():
-                raise LayoutError("the fused blend needs a separate mean buffer (dst) besides the snapshot (src)")
+                err = "live must be a contiguous CUDA tensor shaped like the parameter vector"
+            elif live.dtype != self.src.dtype or live.device.index != self.device:
+                err = "live must match the parameter buffer's dtype and device"
+            elif self.dst.data_ptr() == self.src.data_ptr():
+                err = "the fused blend needs a separate mean buffer (dst) besides the snapshot (src)"
+        # every rank learns every rank's verdict, so all raise together
+        # instead of leaving the others blocked in the next collective
+        votes: list = [None] * self.world
+        dist.all_gather_object(votes, (err, live is not None), group=self.group)
+        errs = [(r, e) for r, (e, _) in enumerate(votes) if e]
+        if errs:
+            raise LayoutError("; ".join(f"rank {r}: {e}" for r, e in errs))
+        if len({bound for _, bound in votes}) != 1:
+            raise ConfigError(f"bind_live is collective: ranks disagree on the fused blend "
+                              f"({[bound for _, bound in votes]})")
         self.plan.bind_live(self.position, None if live is None else live.data_ptr())
         self.live = live
+        self._agree()
+
+    def failed(self) -> bool:
+        """Non-blocking: a cycle of this rank stalled (see ``check``)."""
+        return self.plan.failed()
 
     def average(self, streams=None) -> None:
         """Launch one cycle on ``streams`` (default: the current stream)."""

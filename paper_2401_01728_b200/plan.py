@@ -14,7 +14,8 @@ Reference seam: the per-cycle call is what ``orchestrator._maybe_average``
 from __future__ import annotations
 
 import ctypes
-from typing import Iterable, Sequence
+import os
+from typing import Iterable, Mapping, Sequence
 
 from . import _native as N
 from .errors import ConfigError, LayoutError
@@ -59,6 +60,9 @@ class DevicePlan:
         self._h = h
         self._launch = self.lib.rv_allreduce_mean
         self._stream_cache: dict = {}
+        timeout = os.environ.get("RAVNEST_B200_TIMEOUT_S")  # deployment setting, not a kernel choice
+        if timeout and float(timeout) > 0:
+            self.set_timeout(float(timeout))
 
     @property
     def handle(self):
@@ -95,6 +99,32 @@ class DevicePlan:
 
     def set_push_peers(self, areas: Sequence[int]) -> None:
         N.check(self.lib.rv_plan_set_push_peers(self._h, N.ptr_array(areas)), "rv_plan_set_push_peers")
+
+    def set_option(self, name: str, value: int) -> None:
+        """rv_plan_set_option: ``min_cb``, ``tma``, ``push_items``, ``push_dyn``,
+        ``blend_lag``, ``layout_sms`` (include/ravnest_b200.h RV_OPT_*)."""
+        if name not in N.OPTIONS:
+            raise ConfigError(f"unknown plan option {name!r} (one of {sorted(N.OPTIONS)})")
+        N.check(self.lib.rv_plan_set_option(self._h, N.OPTIONS[name], int(value)), f"rv_plan_set_option({name})")
+
+    def set_options(self, options: Mapping[str, int] | None) -> None:
+        for name, value in (options or {}).items():
+            self.set_option(name, value)
+
+    def prepare(self) -> None:
+        """Build the device tables now (every position bound)."""
+        N.check(self.lib.rv_plan_prepare(self._h), "rv_plan_prepare")
+
+    def layout(self) -> tuple[int, int, int, int]:
+        """(vectors per unit, staging stride, unit slots, work items per lane)
+        of the built tables; push / LL ranks must agree on it."""
+        out = (ctypes.c_int64 * 4)()
+        N.check(self.lib.rv_plan_layout(self._h, out), "rv_plan_layout")
+        return tuple(int(v) for v in out)
+
+    def failed(self) -> bool:
+        """Non-blocking: a cycle of this plan hit its stall timeout."""
+        return bool(self.lib.rv_plan_failed(self._h))
 
     def set_max_blocks(self, n: int) -> None:
         N.check(self.lib.rv_plan_set_max_blocks(self._h, int(n)), "rv_plan_set_max_blocks")
@@ -139,6 +169,13 @@ class DevicePlan:
         N.check(self.lib.rv_allreduce_mean_host(self._h, N.ptr_array(host_src), N.ptr_array(host_dst),
                                                 N.ptr_array(hs), len(hs)), "rv_allreduce_mean_host")
 
+    def run_host_lanes(self, first: int, count: int, host_src: Sequence[int], host_dst: Sequence[int],
+                       streams: Sequence = (None,)) -> None:
+        hs = [_stream_handle(s) for s in streams] or [0]
+        N.check(self.lib.rv_allreduce_mean_host_lanes(self._h, int(first), int(count), N.ptr_array(host_src),
+                                                      N.ptr_array(host_dst), N.ptr_array(hs), len(hs)),
+                "rv_allreduce_mean_host_lanes")
+
     def status(self) -> tuple[int, str]:
         buf = ctypes.create_string_buffer(512)
         rc = self.lib.rv_plan_status(self._h, buf, len(buf))
@@ -174,7 +211,8 @@ class LocalRingGroup:
     """
 
     def __init__(self, starts: Sequence[int], lens: Sequence[int], total: int, devices: Sequence[int],
-                 dtype, acc: str = "f64", lanes: int = 1, protocol: str = "pull"):
+                 dtype, acc: str = "f64", lanes: int = 1, protocol: str = "pull",
+                 options: Mapping[str, int] | None = None):
         self.starts = [int(s) for s in starts]
         self.lens = [int(n) for n in lens]
         self.total = int(total)
@@ -195,6 +233,7 @@ class LocalRingGroup:
         for d in self.device_order:
             plan = DevicePlan(d, self.n_clusters, self.starts, self.lens, self.total, self.dtype_code, acc)
             plan.set_local([m for m, dev in enumerate(self.devices) if dev == d])
+            plan.set_options(options)
             if lanes != 1:
                 plan.set_lanes(lanes)
             self.plans[d] = plan

@@ -65,6 +65,10 @@ def _controller_class(wrap):
         def handle(self, msg, now):
             return super().handle(msg, now)
 
+        @wrap
+        def done(self):
+            return super().done()
+
     return AllReduceController
 
 

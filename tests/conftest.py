@@ -11,18 +11,37 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 REFERENCE_SRC = "/root/reference/pkg/src"  # dev container only; absent on GPU boxes
+REFERENCE_INSTALL = os.path.join(ROOT, "baseline", "_ref")  # offline install; travels to the GPU box
+
+
+def reference_path():
+    """Where the unmodified reference can be imported from: the offline
+    install in baseline/_ref (dev container and GPU box), else the read-only
+    tree of the dev container; None when neither exists."""
+    for path in (REFERENCE_INSTALL, REFERENCE_SRC):
+        if os.path.isdir(os.path.join(path, "ravnest")):
+            return path
+    return None
 
 
 def import_reference(module: str = "ravnest"):
-    """The unmodified reference (CPU checks in the dev container), or skip."""
-    if not os.path.isdir(REFERENCE_SRC):
-        pytest.skip("reference not present here")
+    """The unmodified reference package (CPU checks, the seam tests), or skip."""
+    path = reference_path()
+    if path is None:
+        pytest.skip("reference not present here (baseline/_ref not installed)")
     sys.dont_write_bytecode = True
-    if REFERENCE_SRC not in sys.path:
-        sys.path.append(REFERENCE_SRC)
+    if path not in sys.path:
+        sys.path.append(path)
     import importlib
 
     return importlib.import_module(module)
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 def pytest_configure(config):

@@ -16,6 +16,9 @@ sys.path.insert(0, ROOT)
 from oracle import ring_oracle  # noqa: E402
 from paper_2401_01728_b200.dist import DistRingGroup  # noqa: E402
 
+# test harness knob: force the CB = 8 / 16 kernel buckets through the plan option
+OPTIONS = {"min_cb": int(os.environ.get("RAVNEST_TEST_MIN_CB", "0"))}
+
 
 def bits(a):
     return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
@@ -36,7 +39,8 @@ def stall_phase(rank, world, local):
         x = torch.full((total,), float(rank), device=f"cuda:{local}")
         mean = torch.empty_like(x) if blend else None
         live = torch.zeros_like(x) if blend else None
-        g = DistRingGroup(src=x, dst=mean, starts=[0, lens[0]], lens=lens, protocol=proto, timeout_s=0.5, live=live)
+        g = DistRingGroup(src=x, dst=mean, starts=[0, lens[0]], lens=lens, protocol=proto, timeout_s=0.5, live=live,
+                          options=OPTIONS)
         if rank == 0:
             g.average()
             torch.cuda.synchronize()
@@ -52,7 +56,7 @@ def stall_phase(rank, world, local):
         g.close()
         # a fresh group works
         x.fill_(float(rank))
-        g = DistRingGroup(src=x, starts=[0, lens[0]], lens=lens, protocol=proto)
+        g = DistRingGroup(src=x, starts=[0, lens[0]], lens=lens, protocol=proto, options=OPTIONS)
         g.average()
         torch.cuda.synchronize()
         g.check()
@@ -90,7 +94,8 @@ def blend_phase(rank, world, local):
             x, mean, live = (b[8:8 + total] for b in bufs)
             x.copy_(torch.from_numpy(snaps[rank]))
             live.copy_(torch.from_numpy(lives[rank]))
-            g = DistRingGroup(src=x, dst=mean, starts=starts, lens=lens, lanes=lanes, protocol=proto, live=live)
+            g = DistRingGroup(src=x, dst=mean, starts=starts, lens=lens, lanes=lanes, protocol=proto, live=live,
+                              options=OPTIONS)
             streams = [torch.cuda.Stream() for _ in range(lanes)]
             for st in streams:
                 st.wait_stream(torch.cuda.current_stream())
@@ -178,7 +183,7 @@ def main():
                 dst = dbuf[8:8 + total]
                 dst.fill_(float("nan"))
             g = DistRingGroup(src=x, dst=dst, starts=starts, lens=lens, cluster_id=cid, acc=acc, lanes=lanes,
-                              protocol=proto)
+                              protocol=proto, options=OPTIONS)
             streams = [torch.cuda.Stream() for _ in range(lanes)]
             for s in streams:
                 s.wait_stream(torch.cuda.current_stream())

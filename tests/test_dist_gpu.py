@@ -29,7 +29,7 @@ def test_dist_ring_group_parity():
 @pytest.mark.parametrize("world,min_cb", [(3, 0), (0, 8), (0, 16)])
 def test_dist_wider_kernel_buckets_and_odd_world(world, min_cb):
     """The CB = 8 / 16 kernel instantiations an 8- or 16-GPU job selects,
-    run here with the box's GPUs (RAVNEST_B200_MIN_CB forces the bucket; the
+    run here with the box's GPUs (the min_cb plan option forces the bucket; the
     kernels loop over the runtime member count), and a 3-rank job (odd C:
     true division, uneven chunks, 2 peers per owner)."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
@@ -39,7 +39,7 @@ def test_dist_wider_kernel_buckets_and_odd_world(world, min_cb):
         pytest.skip(f"needs {n} GPUs")
     env = dict(os.environ, RAVNEST_B200_TIMEOUT_S="10", RAVNEST_DIST_QUICK="1")
     if min_cb:
-        env["RAVNEST_B200_MIN_CB"] = str(min_cb)
+        env["RAVNEST_TEST_MIN_CB"] = str(min_cb)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29540 + min_cb + world),
            os.path.join(ROOT, "tests", "dist_worker.py")]

@@ -148,10 +148,9 @@ def test_misaligned_and_ragged(dtype, c):
 
 
 @pytest.mark.parametrize("min_cb", [8, 16])
-def test_wider_kernel_buckets_same_bits(min_cb, monkeypatch):
+def test_wider_kernel_buckets_same_bits(min_cb):
     # the CB = 8 / 16 instantiations (8- and 16-cluster jobs) run with fewer
-    # members: RAVNEST_B200_MIN_CB forces the bucket at plan build time
-    monkeypatch.setenv("RAVNEST_B200_MIN_CB", str(min_cb))
+    # members: the min_cb plan option forces the bucket at plan build time
     for c in (2, 3, 5):
         lens = [100003, 7, 4096 + 5, 3 * c + 1]
         sched = make_sched(lens, c)
@@ -161,7 +160,8 @@ def test_wider_kernel_buckets_same_bits(min_cb, monkeypatch):
             rows = [rng.normal(0, 3, sched.total_params).astype(np_dt) for _ in range(c)]
             want = np.stack(ring_oracle.ring_mean([r.start for r in sched.rings], lens, rows, acc=acc)).astype(np_dt)
             for offsets in (None, [1] * c, [m % 3 for m in range(c)]):  # TMA, vector pull, scalar pull
-                g = LocalRingGroup([r.start for r in sched.rings], lens, sched.total_params, [0] * c, dtype, acc=acc)
+                g = LocalRingGroup([r.start for r in sched.rings], lens, sched.total_params, [0] * c, dtype, acc=acc,
+                                   options={"min_cb": min_cb})
                 bufs = [torch.full((sched.total_params + 8,), -1234.5, dtype=dtype, device="cuda") for _ in range(c)]
                 off = [0] * c if offsets is None else offsets
                 views = [b[o:o + sched.total_params] for b, o in zip(bufs, off)]

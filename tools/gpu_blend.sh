@@ -9,8 +9,7 @@ TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 for n in 2 4; do
 for cfg in "1 auto" "1 0" "1 64" "1 512" "0 auto"; do
   set -- $cfg
-  if [ $2 = auto ]; then unset RAVNEST_B200_BLEND_LAG; else export RAVNEST_B200_BLEND_LAG=$2; fi
-  timeout 300 $TR --nproc-per-node $n --master-port 2964$n bench.py --gpus $n --workload gpt2 --blend 1 --nccl 0 --fused-blend $1 2>/dev/null | grep '^{' > gpurun_out/blend_n${n}_f$1_l$2.jsonl
+  if [ $2 = auto ]; then LAG=-1; else LAG=$2; fi
+  timeout 300 $TR --nproc-per-node $n --master-port 2964$n bench.py --gpus $n --workload gpt2 --blend 1 --nccl 0 --fused-blend $1 --blend-lag $LAG 2>/dev/null | grep '^{' > gpurun_out/blend_n${n}_f$1_l$2.jsonl
   python -c "import json; d=json.load(open('gpurun_out/blend_n${n}_f$1_l$2.jsonl')); print('n=$n fused=$1 lag=$2', d['value'], d['ms_per_step'], d['avg_kernel_ms'], d['gpu_launches'], d.get('phases_us'))"
 done; done
-unset RAVNEST_B200_BLEND_LAG
