@@ -78,6 +78,39 @@ def rendezvous(mine: dict, group=None) -> tuple[list, list[int], int]:
     return everyone, order, order.index(dist.get_rank(group))
 
 
+def agree_layouts(mine, group=None) -> None:
+    """Collective: every rank's (vectors per unit, staging stride, unit slots,
+    work items) must be identical -- push and LL writers compute the owners'
+    staging addresses and unit flags locally, so a rank with another SM count
+    or option set would corrupt the means or hang.  Raises ConfigError on
+    every rank when they differ."""
+    import torch.distributed as dist
+
+    everyone: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(everyone, tuple(mine), group=group)
+    if any(e != tuple(mine) for e in everyone):
+        raise ConfigError(f"ranks derived different cycle layouts (unit vectors, stride, unit slots, "
+                          f"work items): {everyone}; use the same options on every rank "
+                          f"(e.g. layout_sms for GPUs with different SM counts)")
+
+
+def agree_bind_live(err: str | None, bound: bool, group=None) -> None:
+    """Collective vote of bind_live: every rank learns every rank's verdict,
+    so all raise together (LayoutError for a bad buffer anywhere, ConfigError
+    when some ranks bind and others do not) instead of leaving the others
+    blocked in the next collective or, worse, spinning on mean-delivered
+    flags nobody raises."""
+    import torch.distributed as dist
+
+    votes: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(votes, (err, bool(bound)), group=group)
+    errs = [(r, e) for r, (e, _) in enumerate(votes) if e]
+    if errs:
+        raise LayoutError("; ".join(f"rank {r}: {e}" for r, e in errs))
+    if len({b for _, b in votes}) != 1:
+        raise ConfigError(f"bind_live is collective: ranks disagree on the fused blend ({[b for _, b in votes]})")
+
+
 class DistRingGroup:
     """Collective multi-ring averaging of one CUDA buffer per rank.
 
@@ -186,16 +219,8 @@ class DistRingGroup:
         push and LL writers compute the owners' staging addresses and unit
         flags locally, so a rank with another SM count or option set would
         corrupt the means or hang.  Raises ConfigError on a mismatch."""
-        import torch.distributed as dist
-
         self.plan.prepare()
-        mine = self.plan.layout()
-        everyone: list = [None] * self.world
-        dist.all_gather_object(everyone, mine, group=self.group)
-        if any(e != mine for e in everyone):
-            raise ConfigError(f"ranks derived different cycle layouts (unit vectors, stride, unit slots, "
-                              f"work items): {everyone}; use the same options on every rank "
-                              f"(e.g. layout_sms for GPUs with different SM counts)")
+        agree_layouts(self.plan.layout(), self.group)
 
     def bind_live(self, live) -> None:
         """Fuse the delayed-update blend into every cycle: ``live`` (this
@@ -205,8 +230,6 @@ class DistRingGroup:
         kernel then blends unit by unit as the means land and skips the depart
         barrier, so a rank without the blend would wait for flags nobody
         raises.  Raises ConfigError when the ranks disagree."""
-        import torch.distributed as dist
-
         err = None
         if live is not None:
             if not live.is_cuda or not live.is_contiguous() or live.numel() != self.total:
@@ -215,16 +238,7 @@ class DistRingGroup:
                 err = "live must match the parameter buffer's dtype and device"
             elif self.dst.data_ptr() == self.src.data_ptr():
                 err = "the fused blend needs a separate mean buffer (dst) besides the snapshot (src)"
-        # every rank learns every rank's verdict, so all raise together
-        # instead of leaving the others blocked in the next collective
-        votes: list = [None] * self.world
-        dist.all_gather_object(votes, (err, live is not None), group=self.group)
-        errs = [(r, e) for r, (e, _) in enumerate(votes) if e]
-        if errs:
-            raise LayoutError("; ".join(f"rank {r}: {e}" for r, e in errs))
-        if len({bound for _, bound in votes}) != 1:
-            raise ConfigError(f"bind_live is collective: ranks disagree on the fused blend "
-                              f"({[bound for _, bound in votes]})")
+        agree_bind_live(err, live is not None, self.group)
         self.plan.bind_live(self.position, None if live is None else live.data_ptr())
         self.live = live
         self._agree()

@@ -57,3 +57,54 @@ def test_rendezvous_orders_by_cluster_id():
 def test_rendezvous_rejects_duplicate_ids():
     out = _run(2, [5, 5])
     assert all(o[1] == "ConfigError" for o in out)
+
+
+def _vote_worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_01728_b200.dist import agree_bind_live, agree_layouts
+    from paper_2401_01728_b200.errors import ConfigError, LayoutError
+
+    try:
+        if case == "layout-same":
+            agree_layouts((16384, 435328, 102, 166))
+        elif case == "layout-differ":  # e.g. a rank with another SM count
+            agree_layouts((16384, 435328, 102, 166 if rank == 0 else 83))
+        elif case == "live-all":
+            agree_bind_live(None, True)
+        elif case == "live-some":
+            agree_bind_live(None, rank == 0)
+        elif case == "live-bad":
+            agree_bind_live("live must match the parameter buffer's dtype and device" if rank == 1 else None, True)
+        q.put((rank, "ok"))
+    except ConfigError as e:
+        q.put((rank, "ConfigError", str(e)))
+    except LayoutError as e:
+        q.put((rank, "LayoutError", str(e)))
+    dist.destroy_process_group()
+
+
+def _vote(case, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_vote_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    return sorted(out, key=lambda t: t[0])
+
+
+@pytest.mark.parametrize("case,want", [("layout-same", "ok"), ("layout-differ", "ConfigError"),
+                                       ("live-all", "ok"), ("live-some", "ConfigError"),
+                                       ("live-bad", "LayoutError")])
+def test_collective_agreement_raises_on_every_rank(case, want):
+    """DistRingGroup's layout check and the bind_live vote: every rank ends
+    with the same verdict (no rank left waiting in a collective)."""
+    out = _vote(case)
+    assert [o[1] for o in out] == [want, want], out
+    if want == "LayoutError":
+        assert all("rank 1" in o[2] for o in out)
