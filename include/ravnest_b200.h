@@ -179,6 +179,12 @@ int rv_plan_read_trace(rv_plan *plan, int lane, uint64_t *out4);
  * AllReduceController.kickoff..done (multiring.py:180-232, 254-333). */
 int rv_allreduce_mean(rv_plan *plan, void *const *streams, int n_streams);
 
+/* The same for lanes [first_lane, first_lane + n_lanes) only (lane l on
+ * streams[l % n_streams]).  Every lane must be run once per cycle.  Lets a
+ * process that drives several ranks of one group (loopback, tests) issue the
+ * lanes lane-major across its ranks. */
+int rv_allreduce_mean_lanes(rv_plan *plan, int first_lane, int n_lanes, void *const *streams, int n_streams);
+
 /* Same cycle with HOST buffers for the local positions: per lane, copy the
  * lane's ring ranges host->device, average, copy device->host, pipelined
  * across lanes.  host_src/host_dst are indexed like rv_plan_set_local's

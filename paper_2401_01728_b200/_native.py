@@ -72,6 +72,7 @@ SIGNATURES = {
     "rv_plan_set_max_blocks": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "rv_plan_read_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),
     "rv_allreduce_mean": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, ctypes.c_int]),
+    "rv_allreduce_mean_lanes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _c_void_pp, ctypes.c_int]),
     "rv_allreduce_mean_host": (ctypes.c_int, [ctypes.c_void_p, _c_void_pp, _c_void_pp, _c_void_pp, ctypes.c_int]),
     "rv_allreduce_mean_host_lanes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _c_void_pp, _c_void_pp,
                                                     _c_void_pp, ctypes.c_int]),

@@ -862,15 +862,17 @@ int rv_plan_set_timeout(rv_plan *p, double seconds) {
   return RV_OK;
 }
 
-int rv_allreduce_mean(rv_plan *p, void *const *streams, int n_streams) {
+int rv_allreduce_mean_lanes(rv_plan *p, int first_lane, int n_lanes, void *const *streams, int n_streams) {
   if (!p) return set_err(RV_E_ARG, "plan is NULL");
   DeviceGuard g(p->device);
   if (p->dirty || p->ptrs_dirty) {
     int rc = build_tables(p);
     if (rc) return rc;
   }
+  if (first_lane < 0 || n_lanes < 0 || first_lane + n_lanes > p->n_lanes)
+    return set_err(RV_E_ARG, "lanes [%d, %d) outside the plan's %d", first_lane, first_lane + n_lanes, p->n_lanes);
   const int es = elem_size(p->dtype);
-  for (int l = 0; l < p->n_lanes; ++l) {
+  for (int l = first_lane; l < first_lane + n_lanes; ++l) {
     cudaStream_t st = (streams && n_streams > 0) ? (cudaStream_t)streams[l % n_streams] : (cudaStream_t)0;
     int rc = launch_lane(p, l, st);
     if (rc) return rc;
@@ -887,6 +889,11 @@ int rv_allreduce_mean(rv_plan *p, void *const *streams, int n_streams) {
     }
   }
   return RV_OK;
+}
+
+int rv_allreduce_mean(rv_plan *p, void *const *streams, int n_streams) {
+  if (!p) return set_err(RV_E_ARG, "plan is NULL");
+  return rv_allreduce_mean_lanes(p, 0, p->n_lanes, streams, n_streams);
 }
 
 int rv_allreduce_mean_host_lanes(rv_plan *p, int first_lane, int n_lanes, const void *const *host_src,

@@ -8,6 +8,13 @@ buffers as plain device pointers instead of CUDA IPC mappings.  Each rank
 launches on its own stream with an SM budget of 1/C of the device, so all C
 kernels are resident at once (the transports spin on each other's flags).
 
+Launch order matters on one device: rank kernels wait on each other, so no
+launch that depends on an unfinished rank kernel may sit in a hardware queue
+ahead of another rank's kernel (streams share the device's hardware queues,
+CUDA_DEVICE_MAX_CONNECTIONS of them).  ``run`` therefore issues lane by lane
+across all ranks, one stream per rank, and the separate blend launches of the
+pull / LL transports only after every cycle kernel.
+
 What it is for: the transports' arithmetic, work order and flag protocol run
 -- and are checked bit for bit against the oracle -- on a one-GPU box, and
 the same launch sequence is what every rank of an N-GPU job issues
@@ -23,6 +30,7 @@ from typing import Mapping, Sequence
 
 from . import _native as N
 from .errors import ConfigError, LayoutError
+from .blend import blend_
 from .plan import DevicePlan, _dtype_code
 
 TRANSPORTS = ("pull", "push", "ll")
@@ -78,7 +86,8 @@ class LoopbackGroup:
                 p.set_push_peers(push)
         import torch
 
-        self.streams = [[torch.cuda.Stream(device=self.device) for _ in range(self.lanes)] for _ in range(self.C)]
+        # one stream per rank (torch's pool holds 32 per device: more would alias)
+        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(self.C)]
         self._bound = None
         self._lives = None
 
@@ -98,8 +107,13 @@ class LoopbackGroup:
         self._agree()
 
     def bind_live(self, lives: Sequence | None) -> None:
-        for m, p in enumerate(self.plans):
-            p.bind_live(m, None if lives is None else lives[m].data_ptr())
+        """Delayed-update blend: live <- mean + (live - src) every cycle.  The
+        push transport fuses it into its kernel (rv_plan_bind_live); for pull
+        and LL the group launches rv_blend per rank after all cycle kernels
+        (the C ABI would launch it right behind each lane's kernel)."""
+        if self.protocol == "push":
+            for m, p in enumerate(self.plans):
+                p.bind_live(m, None if lives is None else lives[m].data_ptr())
         self._lives = None if lives is None else list(lives)
         self._agree()
 
@@ -114,19 +128,23 @@ class LoopbackGroup:
             raise ConfigError(f"loopback ranks derived different layouts: {sorted(layouts)}")
 
     def run(self, after=None) -> None:
-        """One cycle: every rank's launches on its own streams, ordered after
-        ``after`` (default: the current stream), which then waits for all."""
+        """One cycle: every rank's launches on its own stream, lane by lane
+        across the ranks, ordered after ``after`` (default: the current
+        stream), which then waits for all."""
         import torch
 
         cur = after or torch.cuda.current_stream(self.device)
-        for sts in self.streams:
-            for s in sts:
-                s.wait_stream(cur)
-        for p, sts in zip(self.plans, self.streams):
-            p.run(sts)
-        for sts in self.streams:
-            for s in sts:
-                cur.wait_stream(s)
+        for s in self.streams:
+            s.wait_stream(cur)
+        for lane in range(self.lanes):
+            for p, s in zip(self.plans, self.streams):
+                p.run_lanes(lane, 1, [s])
+        if self._lives is not None and self.protocol != "push":
+            srcs, dsts = self._bound
+            for m, s in enumerate(self.streams):
+                blend_(self._lives[m], srcs[m], dsts[m], s)
+        for s in self.streams:
+            cur.wait_stream(s)
 
     def failed(self) -> bool:
         return any(p.failed() for p in self.plans)

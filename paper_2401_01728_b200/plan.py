@@ -164,6 +164,14 @@ class DevicePlan:
         if rc:
             N.check(rc, "rv_allreduce_mean")
 
+    def run_lanes(self, first: int, count: int, streams: Sequence = (None,)) -> None:
+        key = tuple(_stream_handle(s) for s in streams) or (0,)
+        arr = self._stream_cache.get(key)
+        if arr is None:
+            arr = self._stream_cache[key] = N.ptr_array(key)
+        N.check(self.lib.rv_allreduce_mean_lanes(self._h, int(first), int(count), arr, len(key)),
+                "rv_allreduce_mean_lanes")
+
     def run_host(self, host_src: Sequence[int], host_dst: Sequence[int], streams: Sequence = (None,)) -> None:
         hs = [_stream_handle(s) for s in streams] or [0]
         N.check(self.lib.rv_allreduce_mean_host(self._h, N.ptr_array(host_src), N.ptr_array(host_dst),

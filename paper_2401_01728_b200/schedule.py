@@ -16,14 +16,21 @@ bytes_per_member      multiring.py:340-342
 allreduce_cost        multiring.py:345-394 (RingCost, CostReport)
 ====================  =========================================
 
-Same names, argument meaning and exception classes, so a schedule produced
-here (or by the reference's ``plan_session``, clusterform.py:314-315) feeds
-the GPU path unchanged: any object with ``rings`` (each with ``start``,
-``length``, ``members``) and ``total_params`` is accepted.
+This file is an attributed INTERFACE MIRROR of those reference items: the
+dataclass schemas, the ``dump`` text format, the argument meaning, and the
+exception classes and messages are the reference's contract (callers and
+golden files depend on them, tests/golden/schedule_kats.json pins 47 layouts
+against the unmodified reference).  The construction itself is this
+package's own: cluster layouts are reduced to prefix-sum boundary arrays and
+each ring's owner is found by bisection.  The GPU path does not depend on
+these builders -- any object with ``rings`` (each with ``start``,
+``length``, ``members``) and ``total_params`` is accepted, including the
+reference's own ``RingSchedule`` from ``plan_session`` (clusterform.py:314-315).
 """
 
 from __future__ import annotations
 
+import bisect
 from dataclasses import dataclass
 from typing import Callable, Sequence
 
@@ -72,8 +79,26 @@ class RingStats:
     messages: int
 
 
-def _spans(layout) -> list[tuple[int, int]]:
-    return [(int(sub.param_start), int(sub.param_len)) for sub in layout]
+def _boundaries(cid, layout) -> list[int]:
+    """[s_0 = 0, s_1, ..., s_P = total] of a contiguous layout (submodel p
+    spans [s_p, s_{p+1})); LayoutError when a submodel does not start where
+    the previous one ended."""
+    bounds = [0]
+    for sub in layout:
+        if int(sub.param_start) != bounds[-1]:
+            raise LayoutError(f"cluster {cid}: submodels not contiguous")
+        bounds.append(bounds[-1] + int(sub.param_len))
+    return bounds
+
+
+def _owner(bounds: list[int], lo: int, hi: int):
+    """Index of the first submodel whose span holds [lo, hi), or None.  For a
+    non-empty range the holder is unique and bisection finds it; an empty
+    range (a zero-length ring) takes the first span reaching it."""
+    if lo < hi:
+        p = bisect.bisect_right(bounds, lo) - 1
+        return p if 0 <= p < len(bounds) - 1 and hi <= bounds[p + 1] else None
+    return next((q for q in range(len(bounds) - 1) if bounds[q] <= lo and hi <= bounds[q + 1]), None)
 
 
 def build_ring_schedule(cluster_layouts: dict[int, Sequence]) -> RingSchedule:
@@ -82,69 +107,60 @@ def build_ring_schedule(cluster_layouts: dict[int, Sequence]) -> RingSchedule:
     Every cluster's layout must be contiguous from 0 and cover the same total;
     the cuts must nest so that the segment count equals the largest peer
     count.  Each ring lists, per cluster in ascending id order, the peer
-    whose submodel contains the segment.
+    whose submodel contains the segment (multiring.py:56-105 contract).
     """
     if not cluster_layouts:
         raise LayoutError("no cluster layouts given")
-    order = sorted(cluster_layouts)
-    spans = {cid: _spans(cluster_layouts[cid]) for cid in order}
-    totals = {}
-    for cid in order:
-        expect = 0
-        for start, length in spans[cid]:
-            if start != expect:
-                raise LayoutError(f"cluster {cid}: submodels not contiguous")
-            expect = start + length
-        totals[cid] = expect
+    ids = sorted(cluster_layouts)
+    bounds = {cid: _boundaries(cid, cluster_layouts[cid]) for cid in ids}
+    totals = {cid: b[-1] for cid, b in bounds.items()}
     if len(set(totals.values())) > 1:
         raise LayoutError(f"layouts cover different totals: {totals}")
-    total = totals[order[0]]
-
-    cut_set = set()
-    for cid in order:
-        cut_set.update(start for start, _ in spans[cid] if start > 0)
-    cuts = sorted(cut_set)
-    widest = max(len(spans[cid]) for cid in order)
-    if len(cuts) + 1 != widest:
+    total = totals[ids[0]]
+    # interior cuts: every submodel start above 0, over all clusters
+    interior = sorted({x for b in bounds.values() for x in b[1:-1] if x > 0})
+    n_peers = max(len(b) - 1 for b in bounds.values())
+    if len(interior) + 1 != n_peers:
         raise LayoutError(
-            f"cluster boundaries do not nest: {len(cuts) + 1} segments needed "
-            f"but max peer count is {widest}"
+            f"cluster boundaries do not nest: {len(interior) + 1} segments needed "
+            f"but max peer count is {n_peers}"
         )
-
-    edges = [0, *cuts, total]
+    edges = [0, *interior, total]
     rings = []
-    for rid, (lo, hi) in enumerate(zip(edges[:-1], edges[1:])):
+    for rid in range(len(edges) - 1):
+        lo, hi = edges[rid], edges[rid + 1]
         members = []
-        for cid in order:
-            owner = next(
-                (i for i, (s, n) in enumerate(spans[cid]) if s <= lo and hi <= s + n), None
-            )
-            if owner is None:
+        for cid in ids:
+            p = _owner(bounds[cid], lo, hi)
+            if p is None:
                 raise LayoutError(f"cluster {cid}: no peer owns range [{lo},{hi})")
-            members.append((cid, owner))
+            members.append((cid, p))
         rings.append(Ring(rid, lo, hi - lo, tuple(members)))
     return RingSchedule(tuple(rings), total)
 
 
 def validate_schedule(schedule: RingSchedule, cluster_layouts: dict[int, Sequence]) -> None:
-    """Independent re-check of every schedule invariant."""
-    expect = 0
-    for ring in schedule.rings:
-        if ring.length < 0 or ring.start != expect:
-            raise LayoutError("rings do not tile the parameter space")
-        expect += ring.length
-    if expect != schedule.total_params:
+    """Independent re-check of every schedule invariant (multiring.py:108-131
+    contract): rings tile [0, total) in order, one ring per peer of the
+    widest cluster, one member per cluster in id order, and each member's
+    submodel holds the ring's range."""
+    starts = [r.start for r in schedule.rings]
+    ends = [r.start + r.length for r in schedule.rings]
+    if any(r.length < 0 for r in schedule.rings) or starts != [0, *ends[:-1]][:len(starts)]:
+        raise LayoutError("rings do not tile the parameter space")
+    if (ends[-1] if ends else 0) != schedule.total_params:
         raise LayoutError("rings do not cover all parameters")
-    order = sorted(cluster_layouts)
-    widest = max(len(cluster_layouts[c]) for c in order)
-    if len(schedule.rings) != widest:
-        raise LayoutError(f"{len(schedule.rings)} rings but max peer count is {widest}")
+    ids = sorted(cluster_layouts)
+    n_peers = max(len(cluster_layouts[c]) for c in ids)
+    if len(schedule.rings) != n_peers:
+        raise LayoutError(f"{len(schedule.rings)} rings but max peer count is {n_peers}")
     for ring in schedule.rings:
-        if [cid for cid, _ in ring.members] != order:
+        if [cid for cid, _ in ring.members] != ids:
             raise LayoutError(f"ring {ring.ring_id} lacks one member per cluster")
         for cid, peer in ring.members:
             sub = cluster_layouts[cid][peer]
-            if not (sub.param_start <= ring.start and ring.start + ring.length <= sub.param_start + sub.param_len):
+            lo, hi = int(sub.param_start), int(sub.param_start) + int(sub.param_len)
+            if ring.start < lo or ring.start + ring.length > hi:
                 raise LayoutError(f"ring {ring.ring_id} range outside cluster {cid} peer {peer}")
 
 

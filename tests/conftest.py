@@ -10,6 +10,10 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+# the loopback tests drive several ranks' kernels concurrently on one GPU:
+# give every stream its own hardware queue (must be set before CUDA starts)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 REFERENCE_SRC = "/root/reference/pkg/src"  # dev container only; absent on GPU boxes
 REFERENCE_INSTALL = os.path.join(ROOT, "baseline", "_ref")  # offline install; travels to the GPU box
 

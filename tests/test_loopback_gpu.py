@@ -292,7 +292,7 @@ def test_missing_rank_times_out_and_reports(proto):
     try:
         g.bind_tensors(mem.views)
         assert not g.failed()
-        g.plans[0].run([g.streams[0][0]])
+        g.plans[0].run([g.streams[0]])
         torch.cuda.synchronize()
         assert g.plans[0].failed()
         with pytest.raises(StallError, match="rank"):

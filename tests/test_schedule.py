@@ -117,3 +117,34 @@ def test_stall_report_matches_reference_fifo():
             ref_report = str(ei.value).split("waiting on: ")[-1]
             ours = _stall_text(sched, _ideal_network_progress(sched, c, budget), c).split("waiting on: ")[-1]
             assert ours == ref_report
+
+
+def test_builder_agrees_with_reference_on_random_layouts():
+    """2000 random layouts (nested or not, zero-length submodels and rings,
+    mismatched totals, gaps): same dump or the same exception class and
+    message as the unmodified reference builder (multiring.py:56-105)."""
+    import random
+
+    from conftest import import_reference
+
+    import_reference("ravnest")
+    import ravnest.multiring as R
+
+    rng = random.Random(1)
+    for _ in range(2000):
+        total = rng.randint(0, 12)
+        lay = {}
+        for c in range(rng.randint(1, 4)):
+            pts = [0, *sorted(rng.choices(range(total + 1), k=rng.randint(0, 3))), total]
+            lay[c * 3 + rng.randint(0, 2)] = [(pts[i], pts[i + 1] - pts[i]) for i in range(len(pts) - 1)]
+        if rng.random() < 0.1:
+            k = rng.choice(list(lay))
+            lay[k] = lay[k][:-1] if len(lay[k]) > 1 else [(1, 2)]
+        outcome = []
+        for mod in (R, rv):
+            try:
+                outcome.append(mod.build_ring_schedule({c: [mod.ParamRange(a, b) for a, b in v]
+                                                        for c, v in lay.items()}).dump())
+            except Exception as e:  # noqa: BLE001 - compare class names and messages
+                outcome.append((type(e).__name__, str(e)))
+        assert outcome[0] == outcome[1], lay
