@@ -476,18 +476,23 @@ int build_tables(rv_plan *p) {
   // another on this device while both wait on peers)
   int64_t capacity = (int64_t)p->sm_count * p->occ;
   if (p->max_blocks > 0) capacity = std::min<int64_t>(capacity, p->max_blocks);
+  // Multi-rank lanes spin on their peers, so all lanes of a cycle must be
+  // resident together: the budget is split in proportion to lane bytes.  A
+  // co-resident plan (no peers) has no such constraint, and its lanes often
+  // run one after another (the host-buffer pipeline staggers them behind
+  // their copies), so every lane gets the whole budget.
   std::vector<int64_t> share(p->n_lanes);
   int64_t granted = 0;
   for (int l = 0; l < p->n_lanes; ++l) {
     const rv_plan::Lane &lane = p->lanes[l];
     int64_t sh = all_elems > 0 ? capacity * lane.elems / all_elems : 0;
-    if (p->n_lanes == 1) sh = capacity;
+    if (p->n_lanes == 1 || p->n_ranks == 1) sh = capacity;
     share[l] = std::max<int64_t>(1, std::min<int64_t>(sh, std::max<int64_t>(1, lane.n_tiles)));
     granted += share[l];
   }
   // the one-block floor of small lanes must not push the sum past the
   // budget (lanes spin on peers: every block of every lane must be resident)
-  while (granted > capacity) {
+  while (p->n_ranks > 1 && granted > capacity) {
     int big = 0;
     for (int l = 1; l < p->n_lanes; ++l)
       if (share[l] > share[big]) big = l;
