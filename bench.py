@@ -31,6 +31,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# per-lane streams of one cycle must not share hardware queues (set before CUDA starts)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 # tensor-boundary ring lengths (torchvision / transformers shapes)
 WORKLOADS = {
