@@ -456,7 +456,7 @@ int build_tables(rv_plan *p) {
       lane.blend_lag = p->blend_lag_opt >= 0 ? p->blend_lag_opt
                                              : (2 * (int64_t)p->sm_count * p->occ + p->C - 1) / p->C;
       lane.n_tiles = ll ? (int64_t)(p->C - 1) * lane.scatter_umax * 2 + lane.ounits[p->rank]
-                        : (int64_t)(p->fused_blend ? 3 * p->C - 1 : p->C) * lane.umax_all;
+                        : (int64_t)(p->fused_blend ? 2 * p->C - 1 : p->C) * lane.umax_all;
       lane.nseg = (int)segs.size();
       int rc = upload(lane, segs, {});
       if (rc) return rc;
@@ -963,8 +963,7 @@ int rv_plan_status(rv_plan *p, char *diag, size_t diag_len) {
   std::string rings;
   if (lane < p->lanes.size())
     for (int r : p->lanes[lane].rings) rings += (rings.empty() ? "" : "|") + std::to_string(r);
-  const char *ph = phase == 0 ? "arrive" : phase == 1 ? "depart" : phase == 2 ? "unit"
-                 : phase == 3 ? "mean-delivered" : "local delta";
+  const char *ph = phase == 0 ? "arrive" : phase == 1 ? "depart" : phase == 2 ? "unit" : "mean-delivered";
   if (diag && diag_len)
     snprintf(diag, diag_len, "waiting on: (ring=%s, phase=%s, rank=%u)", rings.empty() ? "?" : rings.c_str(), ph,
              peer);

@@ -62,8 +62,6 @@ struct LaneState {
   unsigned long long signaled;  // last epoch whose arrive flags were posted
   unsigned int done;            // blocks finished in the running cycle
   unsigned int grab;            // push: work items handed out beyond the first one per block
-  unsigned int deltas;          // push, fused blend: delta items finished in the running cycle
-  unsigned int pad_;
 };
 
 struct CycleParams {
@@ -207,7 +205,6 @@ __device__ void depart(const CycleParams &p, unsigned long long epoch, bool cros
       trace_max(p, 3);
       p.state->done = 0u;
       p.state->grab = 0u;
-      p.state->deltas = 0u;
       *(volatile unsigned long long *)&p.state->epoch = epoch;
       __threadfence();
     }

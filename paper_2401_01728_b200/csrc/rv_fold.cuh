@@ -54,25 +54,9 @@ __device__ __forceinline__ T blend_one(T mean, T live, T snap) {
   return lb == sb ? mean : mean + (live - snap);
 }
 
-// The push transport's fused blend runs in two halves.  While the chunks
-// are still being scattered (NVLink busy, HBM mostly idle) a delta item
-// turns live into delta(live, snap); once the means are in, the blend is
-// live <- mean + live.  delta() stores -0.0 where live and snap are the same
-// bits, and mean + (-0.0) == mean for every mean (RN mode, -0.0 included),
-// so the two halves are bit for bit blend_one(mean, live, snap): one IEEE
-// subtract and one IEEE add, exactly as in the one-pass blend.
-template <typename T>
-__device__ __forceinline__ T blend_delta(T live, T snap) {
-  using U = typename std::conditional<sizeof(T) == 8, unsigned long long, unsigned>::type;
-  U lb, sb;
-  memcpy(&lb, &live, sizeof(T));
-  memcpy(&sb, &snap, sizeof(T));
-  return lb == sb ? (T)-0.0 : live - snap;
-}
-
 // Fold of one element (chunk edges, misaligned buffers): ring order from s.k.
-// Push with the fused blend: the owner (s.k == me) also finishes its own live
-// value (live already holds the delta, see blend_delta).
+// Push with the fused blend: the owner (s.k == me) also blends its own live
+// value, its snapshot being the first member folded.
 template <typename T, typename Acc, bool PUSH>
 __device__ __forceinline__ void fold_scalar(const CycleParams &p, const Seg &s, int64_t i) {
   int m = s.k;
@@ -86,7 +70,7 @@ __device__ __forceinline__ void fold_scalar(const CycleParams &p, const Seg &s, 
   for (int q = 0; q < p.C; ++q) __stcs(static_cast<T *>(p.dst[q]) + i, out);
   if (PUSH && p.live_me) {
     T *live = static_cast<T *>(p.live_me) + i;
-    *live = out + *live;
+    *live = blend_one<T>(out, *live, first);
   }
 }
 
@@ -130,12 +114,12 @@ __device__ __forceinline__ void fold_pass(const CycleParams &p, const Seg &s, in
 #pragma unroll
       for (int q = 0; q < CB; ++q)
         if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
-      if (PUSH && p.live_me) {  // fused blend, second half, on the owner's own copy
+      if (PUSH && p.live_me) {  // fused blend of the owner's own copy (x[u][0] is its snapshot)
         Raw *lp = reinterpret_cast<Raw *>(static_cast<T *>(p.live_me) + i);
         Lanes<T, VB> l;
         l.raw = *lp;
 #pragma unroll
-        for (int e = 0; e < N; ++e) l.v[e] = out.v[e] + l.v[e];
+        for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(out.v[e], l.v[e], x[u][0].v[e]);
         *lp = l.raw;
       }
     }

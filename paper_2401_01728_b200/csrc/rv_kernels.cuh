@@ -124,42 +124,9 @@ __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
   return segs[a];
 }
 
-// Push with the fused blend, first half: unit u of owner q's chunk in this
-// rank's buffers, live <- delta(live, snap) (blend_delta).  No dependency:
-// these items run in the scatter phase, when HBM is mostly idle.
-template <typename T, int VB>
-__device__ void delta_item(const CycleParams &p, int q, int64_t u) {
-  constexpr int N = VB / sizeof(T);
-  using Raw = typename RawVec<VB>::type;
-  if (u >= p.ounits[q]) return;
-  const Seg s = find_unit<T>(p.segs + p.oseg_base[q], p.oseg_base[q + 1] - p.oseg_base[q], u);
-  const int64_t uu = u - s.unit0;
-  const int64_t nvec = (s.body_hi - s.body_lo) / N;
-  const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
-  const T *snap = static_cast<const T *>(p.src[p.me]);
-  T *live = static_cast<T *>(p.live_me);
-  for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
-    const int64_t i = s.body_lo + j * N;
-    Lanes<T, VB> l, sn;
-    sn.raw = *reinterpret_cast<const Raw *>(snap + i);  // the scatter / fold read it again: keep it in L2
-    l.raw = *reinterpret_cast<const Raw *>(live + i);
-#pragma unroll
-    for (int e = 0; e < N; ++e) l.v[e] = blend_delta<T>(l.v[e], sn.v[e]);
-    *reinterpret_cast<Raw *>(live + i) = l.raw;
-  }
-  if (uu == 0) {
-    const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
-    if ((int64_t)threadIdx.x < nhead + ntail) {
-      const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x : s.body_hi + ((int64_t)threadIdx.x - nhead);
-      live[i] = blend_delta<T>(live[i], snap[i]);
-    }
-  }
-}
-
-// Push with the fused blend, second half: unit u of owner q, once q's
-// mean-delivered flag for it is set: live <- mean + live over the unit's
-// range of this rank's buffers (live holds the delta).  False when the cycle
-// failed (block must stop).
+// Push with the fused blend: unit u of owner q, once q's mean-delivered flag
+// for it is set: live <- mean + (live - snap) over the unit's range of this
+// rank's buffers.  False when the cycle failed (block must stop).
 template <typename T, int VB>
 __device__ bool blend_item(const CycleParams &p, int q, int64_t u, unsigned long long epoch, unsigned long long t0,
                            int *s_ok) {
@@ -179,44 +146,26 @@ __device__ bool blend_item(const CycleParams &p, int q, int64_t u, unsigned long
   const int64_t nvec = (s.body_hi - s.body_lo) / N;
   const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
   const T *mean = static_cast<const T *>(p.dst[me]);
+  const T *snap = static_cast<const T *>(p.src[me]);
   T *live = static_cast<T *>(p.live_me);
   for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
     const int64_t i = s.body_lo + j * N;
-    Lanes<T, VB> m, l;
+    Lanes<T, VB> m, l, sn;
     m.raw = __ldcg(reinterpret_cast<const Raw *>(mean + i));
-    l.raw = __ldcs(reinterpret_cast<const Raw *>(live + i));
+    sn.raw = __ldcs(reinterpret_cast<const Raw *>(snap + i));
+    l.raw = *reinterpret_cast<const Raw *>(live + i);
 #pragma unroll
-    for (int e = 0; e < N; ++e) l.v[e] = m.v[e] + l.v[e];
-    __stcs(reinterpret_cast<Raw *>(live + i), l.raw);
+    for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(m.v[e], l.v[e], sn.v[e]);
+    *reinterpret_cast<Raw *>(live + i) = l.raw;
   }
   if (uu == 0) {
     const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
     if ((int64_t)threadIdx.x < nhead + ntail) {
       const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x : s.body_hi + ((int64_t)threadIdx.x - nhead);
-      live[i] = __ldcg(mean + i) + live[i];
+      live[i] = blend_one<T>(__ldcg(mean + i), live[i], snap[i]);
     }
   }
   return true;
-}
-
-// Fused blend: before the first fold or blend item a block waits until every
-// delta item of the cycle is done (they all precede it in the work order and
-// have no dependencies, so this never waits on another rank).
-__device__ __forceinline__ bool await_deltas(const CycleParams &p, unsigned total, int *s_ok) {
-  if (threadIdx.x == 0) {
-    unsigned spins = 0;
-    const unsigned long long t0 = globaltimer();
-    while (*(volatile unsigned *)&p.state->deltas < total) {
-      if ((++spins & 255u) == 0 && globaltimer() - t0 > p.timeout_ns) {
-        fail(p, (4u << 16) | ((unsigned)p.lane << 8) | (unsigned)p.me);
-        *s_ok = 0;
-        break;
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-  return *s_ok != 0;
 }
 
 template <typename T, typename Acc, int CB, int VB, int U>
@@ -237,58 +186,37 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
   const unsigned long long epoch = s_epoch;
   const int C = p.C, me = p.me;
   // Work order (identical on every rank): every scatter item (unit-major),
-  // then every fold item.  With the fused blend, each unit of the head also
-  // carries C delta items (the blend's first half, one per owner's chunk of
-  // this rank's buffers), and the folds come in groups of C items: group g =
-  // fold unit g, then the blend items of unit g - blend_lag of the C - 1
-  // other owners (each waits for that owner's mean-delivered flag, set by a
-  // fold item blend_lag groups earlier), so the blend's HBM traffic runs
-  // under the NVLink traffic of the scatter and of later folds, and finds the
-  // means in L2.  Items wait only on items at earlier positions (of other
-  // ranks, or this rank's delta items), and blocks take items in position
-  // order, so a co-resident grid always drains.
+  // then every fold item.  With the fused blend the folds come in groups of
+  // C items: group g = fold unit g, then the blend items of unit
+  // g - blend_lag of the C - 1 other owners (each waits for that owner's
+  // mean-delivered flag, set by a fold item blend_lag groups earlier), so
+  // the blend's HBM traffic runs under the NVLink traffic of later folds
+  // and finds the means in L2.  Items wait only on items at earlier
+  // positions (of other ranks), and blocks take items in position order,
+  // so a co-resident grid always drains.
   const int64_t ua = p.umax_all;
   const bool fused = p.live_me != nullptr;
   const int64_t blag = p.blend_lag;
-  const int64_t hstride = fused ? 2 * C - 1 : C - 1;  // head items per unit
-  const int64_t head = ua * hstride;
-  const unsigned n_deltas = fused ? (unsigned)(ua * C) : 0u;
+  const int64_t head = ua * (C - 1);
   const int64_t n_work = fused ? head + (ua + blag) * C : ua * C;
   const unsigned long long t0 = globaltimer();
   __shared__ long long s_next;
-  bool deltas_seen = !fused;
 
   for (int64_t w = blockIdx.x; w < n_work; w = p.push_dyn ? grab_next(p, &s_next) : w + gridDim.x) {
     if (!s_ok) break;
     int64_t sidx = -1, fidx = -1;  // scatter item (unit * (C-1) + peer) or fold unit
     if (w < head) {
-      const int64_t u = w / hstride, r = w % hstride;
-      if (r < C - 1) {
-        sidx = u * (C - 1) + r;
-      } else {
-        // delta item: unit u of owner (r - (C - 1)), counted when done
-        delta_item<T, VB>(p, (int)(r - (C - 1)), u);
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(&p.state->deltas, 1u);
-        continue;
-      }
+      sidx = w;
+    } else if (!fused) {
+      fidx = w - head;
+    } else if ((w - head) % C == 0) {
+      fidx = (w - head) / C;
     } else {
-      if (!deltas_seen) {
-        if (!await_deltas(p, n_deltas, &s_ok)) break;
-        deltas_seen = true;
-      }
-      if (!fused) {
-        fidx = w - head;
-      } else if ((w - head) % C == 0) {
-        fidx = (w - head) / C;
-      } else {
-        // blend item: unit u of owner q, from q's means in this rank's dst
-        const int r = (int)((w - head) % C) - 1;
-        const int64_t u = (w - head) / C - blag;
-        if (!blend_item<T, VB>(p, me + 1 + r < C ? me + 1 + r : me + 1 + r - C, u, epoch, t0, &s_ok)) break;
-        continue;
-      }
+      // blend item: unit u of owner q, from q's means in this rank's dst
+      const int r = (int)((w - head) % C) - 1;
+      const int64_t u = (w - head) / C - blag;
+      if (!blend_item<T, VB>(p, me + 1 + r < C ? me + 1 + r : me + 1 + r - C, u, epoch, t0, &s_ok)) break;
+      continue;
     }
     if (sidx >= 0) {
       const int r = (int)(sidx % (C - 1));

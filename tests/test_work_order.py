@@ -5,24 +5,18 @@ order always drain (push transport).  CPU only."""
 
 import random
 
-import numpy as np
 import pytest
-
-from oracle import ring_oracle
 
 
 def work_order(C, ua, blag, fused):
     """Position -> item, as the kernel maps it: ('s', unit, peer) scatter,
-    ('d', unit, owner) delta (fused blend, first half), ('f', unit) fold,
-    ('b', unit, peer) blend of another owner's unit (second half)."""
-    hstride = 2 * C - 1 if fused else C - 1
-    head = ua * hstride
+    ('f', unit) fold, ('b', unit, peer) blend of another owner's unit."""
+    head = ua * (C - 1)
     n = head + (ua + blag) * C if fused else ua * C
     out = []
     for w in range(n):
         if w < head:
-            u, r = divmod(w, hstride)
-            out.append(("s", u, r) if r < C - 1 else ("d", u, r - (C - 1)))
+            out.append(("s", w // (C - 1), w % (C - 1)))
         elif not fused:
             out.append(("f", w - head))
         elif (w - head) % C == 0:
@@ -46,13 +40,10 @@ def test_every_item_once_and_dependencies_earlier(fused):
             assert item not in pos
             pos[item] = w
         scatters = [k for k in pos if k[0] == "s"]
-        deltas = [k for k in pos if k[0] == "d"]
         folds = [k for k in pos if k[0] == "f"]
         blends = [k for k in pos if k[0] == "b"]
         assert len(scatters) == ua * (C - 1) and len(folds) == ua
         assert len(blends) == (ua * (C - 1) if fused else 0)
-        assert len(deltas) == (ua * C if fused else 0)
-        last_delta = max((pos[d] for d in deltas), default=-1)
         for u in range(ua):
             # a fold waits for every peer's scatter of its unit
             assert all(pos[("s", u, r)] < pos[("f", u)] for r in range(C - 1))
@@ -60,35 +51,3 @@ def test_every_item_once_and_dependencies_earlier(fused):
             # map on every rank)
             for r in range(C - 1 if fused else 0):
                 assert pos[("f", u)] < pos[("b", u, r)]
-        # folds and blends (the blend's second half) wait for every delta
-        # item of the rank; all of them sit in the head, before any of those
-        assert all(pos[k] > last_delta for k in folds + blends)
-
-
-def test_split_blend_equals_one_pass_blend():
-    """The fused push blend runs in two halves -- live <- delta(live, snap)
-    in the scatter phase, live <- mean + live once the mean is in -- where
-    delta stores -0.0 for bitwise-equal live and snap.  That is bit for bit
-    the one-pass blend mean + (live - snap), exactly mean where live == snap
-    (oracle.blend), including signed zeros, infinities and NaN."""
-    rng = np.random.Generator(np.random.Philox(key=12))
-    for dt in (np.float32, np.float64):
-        n = 1 << 16
-        snap = rng.normal(0, 1, n).astype(dt)
-        live = snap + rng.normal(0, 1e-3, n).astype(dt)
-        mean = rng.normal(0, 1, n).astype(dt)
-        live[::5] = snap[::5]
-        special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 1.0], dtype=dt)
-        k = len(special)
-        grid = np.array(np.meshgrid(np.arange(k), np.arange(k), np.arange(k))).reshape(3, -1)
-        mean = np.concatenate([mean, special[grid[0]]])
-        live = np.concatenate([live, special[grid[1]]])
-        snap = np.concatenate([snap, special[grid[2]]])
-        ut = {4: np.uint32, 8: np.uint64}[np.dtype(dt).itemsize]
-        with np.errstate(all="ignore"):
-            delta = np.where(live.view(ut) == snap.view(ut), dt(-0.0), live - snap)
-            two_half = mean + delta
-            want = ring_oracle.blend(mean, live, snap)
-        nan = np.isnan(want)
-        assert np.array_equal(np.isnan(two_half), nan)
-        assert np.array_equal(two_half.view(ut)[~nan], want.view(ut)[~nan]), dt
