@@ -435,7 +435,11 @@ int build_tables(rv_plan *p) {
             u += std::max<int64_t>(1, (nvec + unit_vecs - 1) / unit_vecs);
           }
           segs.push_back(s);
-          if (q == p->rank) lane.elems += s.hi - s.lo;
+          // a push / LL rank scatters every other owner's piece of the lane
+          // and folds its own: its work is the whole lane, not its own chunk
+          // (sizing by the own chunk gave a lane holding another owner's
+          // chunk a single block, 36-73 GB/s at lanes > rings)
+          lane.elems += s.hi - s.lo;
         }
         lane.ounits[q] = u;
         if (u > p->units_max) return set_err(RV_E_ARG, "push unit bound exceeded (%lld > %lld)",
