@@ -318,6 +318,10 @@ class LocalRingGroup:
         for plan in self.plans.values():
             plan.check_status()
 
+    def failed(self) -> bool:
+        """Non-blocking: a cycle of one of the plans stalled."""
+        return any(plan.failed() for plan in self.plans.values())
+
     def close(self) -> None:
         for plan in self.plans.values():
             plan.close()
