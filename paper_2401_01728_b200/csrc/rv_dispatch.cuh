@@ -56,8 +56,19 @@ KernelFn pick_cb(int c, bool push, int *u_out) {
 // blocks per SM (0.895 / 0.878 of measured HBM): 0.905-0.933 / 0.919-0.922;
 // 2 x 32/40/48/80/96 KB, 3 x 64 KB, 6 x 32 KB, 8 x 16 KB and L2 evict-first
 // hints were slower (round-1 experiment builds, DESIGN.md tuning table).
-constexpr int kTmaStages = 2;
-constexpr int kTmaStageBytes = 64 * 1024;
+// Round 2, alternating A/B builds (profiles/r02/ab_tma_layouts_n1.txt), BERT
+// / ResNet-50 C=8: 2 x 64 KB 0.947 / 0.932, 3 x 64 KB 0.921 / 0.886,
+// 4 x 48 KB 0.881 / 0.850 of HBM -- more bytes in flight per SM is slower:
+// the pipeline is not latency-bound (the fp32 fold, which skips the f64
+// conversions, is within 0.2%).
+#ifndef RV_TMA_STAGES  // A/B builds only (tools/gpu_ab_tma.sh); the library uses the defaults
+#define RV_TMA_STAGES 2
+#endif
+#ifndef RV_TMA_STAGE_KB
+#define RV_TMA_STAGE_KB 64
+#endif
+constexpr int kTmaStages = RV_TMA_STAGES;
+constexpr int kTmaStageBytes = RV_TMA_STAGE_KB * 1024;
 
 // BL: the fused-blend kernel; a stage carries C src and C live tiles, so the
 // same stage bytes hold half the vectors per member.

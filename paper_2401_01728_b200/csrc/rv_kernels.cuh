@@ -532,13 +532,16 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
   // each thread walks the segment table forward (SegWalk)
   SegWalk walk;
   auto seg_of = [&](int64_t t, int64_t *local) -> const Seg & { return walk.at(p, t, local); };
+  // tiles dealt round-robin (one contiguous run per block measured slower:
+  // 0.940 vs 0.947 of HBM, profiles/r02/ab_tma_layouts_n1.txt)
+  const int64_t TILE_FIRST = blockIdx.x, TILE_END = p.n_tiles, TILE_STEP = gridDim.x;
 
   if (tid < 32) {
     if (tid == 0) {  // producer
       int stage = 0;
       unsigned phase = 0;
       int64_t n = 0;
-      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++n) {
+      for (int64_t t = TILE_FIRST; t < TILE_END; t += TILE_STEP, ++n) {
         int64_t lt;
         const Seg s = seg_of(t, &lt);
         const int64_t nvec = (s.body_hi - s.body_lo) / N;
@@ -571,7 +574,7 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
   int stage = 0;
   unsigned phase = 0;
   int ob = 0;
-  for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+  for (int64_t t = TILE_FIRST; t < TILE_END; t += TILE_STEP) {
     int64_t lt;
     const Seg s = seg_of(t, &lt);
     const int64_t nvec = (s.body_hi - s.body_lo) / N;
