@@ -326,3 +326,8 @@ class LocalRingGroup:
         for plan in self.plans.values():
             plan.close()
         self.plans = {}
+        # drop the buffers kept alive for the plans (and the numpy drop-in's
+        # device staging, multiring._HostCycle) so an evicted group frees them
+        for attr in ("_bound", "_lives", "_host_bufs", "_host_streams"):
+            if hasattr(self, attr):
+                setattr(self, attr, None)
