@@ -27,3 +27,24 @@ def test_reference_arm_line():
     assert "workload" in d["config"]
     with open(os.path.join(ROOT, "BASELINE.json")) as f:
         assert d["metric"] == json.load(f)["metric"]
+
+
+def test_reference_arm_runs_the_unmodified_reference_on_the_full_workload():
+    """With baseline/_ref installed the arm times the unmodified
+    ravnest.multiring.apply_ring_mean on the whole parameter set (here
+    ResNet-50's rings at C=2 to stay quick), capping the step count to its
+    time budget and saying so."""
+    from conftest import reference_path
+
+    import pytest
+
+    if reference_path() is None:
+        pytest.skip("reference not installed")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload",
+                          "resnet50", "--clusters", "2", "--steps", "50", "--warmup", "5", "--ref-budget-s", "3"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    d = json.loads([l for l in res.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["cpu_baseline"]["kind"] == "reference" and "FULL workload" in d["cpu_baseline"]["sample"]
+    assert 1 <= d["steps"] <= d["steps_requested"] == 50
+    assert d["config"]["clusters"] == 2 and d["ms_per_step"] > 0 and d["value"] > 0
