@@ -926,7 +926,7 @@ def main():
     ap.add_argument("--trace", type=int, default=1, help="N>1: add a device-side phase trace")
     ap.add_argument("--numa-bind", type=int, default=1, help="bind ranks to their GPU's NUMA-local CPUs for e2e")
     ap.add_argument("--e2e-lanes", type=int, default=0,
-                    help="pipeline stages of the host-buffer path (0: 16 on one GPU, one per ring across GPUs)")
+                    help="pipeline stages of the host-buffer path (0: 32 on one GPU, one per ring across GPUs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -935,9 +935,11 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     n_gpus = max(world, 1) if world > 1 else args.gpus
     if args.e2e_lanes <= 0:
-        # measured: finer pipelining helps the single-GPU host path (90 -> 82 ms
-        # per BERT step); across GPUs every extra lane adds its own barriers
-        args.e2e_lanes = 16 if world <= 1 else len(WORKLOADS[args.workload])
+        # measured: finer pipelining helps the single-GPU host path (BERT C=8
+        # per step: 8 / 16 / 32 / 64 lanes 79.1 / 76.1-83.8 / 75.8 / 80.4 ms,
+        # profiles/r02/e2e_lanes_n1.txt); across GPUs every extra lane adds
+        # its own barriers
+        args.e2e_lanes = 32 if world <= 1 else len(WORKLOADS[args.workload])
 
     if args.impl == "reference":
         run_reference(args, n_gpus, rank)
