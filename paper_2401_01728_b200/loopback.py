@@ -37,7 +37,9 @@ TRANSPORTS = ("pull", "push", "ll")
 
 
 class LoopbackGroup:
-    """C ranks of one averaging group, all on ``device``.
+    """C ranks of one averaging group, all on ``device`` -- or spread over
+    ``devices`` (rank m on devices[m]; several ranks may share a GPU), which
+    drives an 8-rank group over the NVLink of a 4-GPU box from one process.
 
     Position m (the m-th smallest cluster id) is rank m.  ``bind_tensors``
     takes the C member buffers (rank m averages buffer m in place, or
@@ -48,7 +50,7 @@ class LoopbackGroup:
     def __init__(self, starts: Sequence[int], lens: Sequence[int], total: int, n_ranks: int, dtype,
                  protocol: str = "push", device: int = 0, acc: str = "f64", lanes: int = 1,
                  options: Mapping[str, int] | None = None, timeout_s: float | None = None,
-                 blocks_per_rank: int | None = None):
+                 blocks_per_rank: int | None = None, devices: Sequence[int] | None = None):
         if protocol not in TRANSPORTS:
             raise ConfigError(f"unknown protocol {protocol!r} (one of {TRANSPORTS})")
         if n_ranks < 2 or n_ranks > N.RV_MAX_RANKS:
@@ -57,18 +59,28 @@ class LoopbackGroup:
         self.lens = [int(n) for n in lens]
         self.total = int(total)
         self.C = int(n_ranks)
-        self.device = int(device)
+        # rank m lives on devices[m] (default: all on `device`); ranks on
+        # different devices reach each other's buffers, flags and staging
+        # through peer access over NVLink, like DistRingGroup's IPC mappings
+        self.devices = [int(device)] * self.C if devices is None else [int(d) for d in devices]
+        if len(self.devices) != self.C:
+            raise ConfigError(f"{len(self.devices)} devices for {self.C} ranks")
+        self.device = self.devices[0]
         self.protocol = protocol
         self.lanes = int(lanes)
         lib = N.load()
-        sms = lib.rv_device_sm_count(self.device)
-        # every rank's kernels must be resident together: the cycle kernels
-        # run <= 2 blocks per SM (__launch_bounds__(256, 2)), so 2*SMs/C
-        # blocks per rank leave room for all of them
-        budget = blocks_per_rank or max(1, 2 * sms // self.C)
+        for a in set(self.devices):
+            for b in set(self.devices):
+                if a != b:
+                    N.check(lib.rv_enable_peer_access(a, b), "rv_enable_peer_access")
         self.plans = []
         for m in range(self.C):
-            p = DevicePlan(self.device, self.C, self.starts, self.lens, self.total, _dtype_code(dtype), acc)
+            dev = self.devices[m]
+            # every rank's kernels must be resident together: the cycle
+            # kernels run <= 2 blocks per SM (__launch_bounds__(256, 2)), so
+            # 2*SMs / (ranks on the device) blocks per rank leave room for all
+            budget = blocks_per_rank or max(1, 2 * lib.rv_device_sm_count(dev) // self.devices.count(dev))
+            p = DevicePlan(dev, self.C, self.starts, self.lens, self.total, _dtype_code(dtype), acc)
             p.set_options(options)
             if self.lanes != 1:
                 p.set_lanes(self.lanes)
@@ -87,7 +99,7 @@ class LoopbackGroup:
         import torch
 
         # one stream per rank (torch's pool holds 32 per device: more would alias)
-        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(self.C)]
+        self.streams = [torch.cuda.Stream(device=d) for d in self.devices]
         self._bound = None
         self._lives = None
 
@@ -97,8 +109,9 @@ class LoopbackGroup:
             raise LayoutError(f"expected {self.C} member buffers")
         for m, (s, d) in enumerate(zip(srcs, dsts)):
             for t in (s, d):
-                if not t.is_cuda or t.device.index != self.device or not t.is_contiguous() or t.numel() != self.total:
-                    raise LayoutError(f"member buffer {m} must be a contiguous cuda:{self.device} tensor "
+                if not t.is_cuda or t.device.index != self.devices[m] or not t.is_contiguous() or \
+                        t.numel() != self.total:
+                    raise LayoutError(f"member buffer {m} must be a contiguous cuda:{self.devices[m]} tensor "
                                       f"of {self.total} elements")
         for p in self.plans:
             for m, (s, d) in enumerate(zip(srcs, dsts)):
@@ -156,7 +169,8 @@ class LoopbackGroup:
     def close(self) -> None:
         import torch
 
-        torch.cuda.synchronize(self.device)
+        for d in set(self.devices):
+            torch.cuda.synchronize(d)
         for p in self.plans:
             p.close()
         self.plans = []

@@ -311,3 +311,34 @@ def test_missing_rank_times_out_and_reports(proto):
     finally:
         g.close()
     assert (mem.host() == np.float32(sum(range(c)) / c)).all()
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("proto", ["pull", "push", "ll"])
+def test_ranks_spread_over_devices(proto):
+    """C = 8 rank plans over every visible GPU in one process (two or more
+    ranks per GPU): the 8-rank kernels with real NVLink peer traffic and
+    sys-scope flags between devices, bit-exact against the oracle."""
+    ng = torch.cuda.device_count()
+    if ng < 2:
+        pytest.skip("needs >= 2 GPUs")
+    c = 8
+    devices = [m * ng // c for m in range(c)]
+    for li, lens in enumerate(random_layouts(c)[:2] + [[1 << 20, 77777, 3]]):
+        starts, total = starts_of(lens), sum(lens)
+        rows = [np.random.Generator(np.random.Philox(key=4000 * li + m)).normal(0, 1, total).astype(np.float32)
+                for m in range(c)]
+        want = np.stack(ring_oracle.ring_mean(starts, lens, rows)).astype(np.float32)
+        xs = [torch.from_numpy(r).to(f"cuda:{d}") for r, d in zip(rows, devices)]
+        g = LoopbackGroup(starts, lens, total, c, torch.float32, protocol=proto, devices=devices, timeout_s=TIMEOUT_S)
+        try:
+            g.bind_tensors(xs)
+            for _ in range(2):  # two cycles: epochs and staging reuse across devices
+                g.run()
+            for d in set(devices):
+                torch.cuda.synchronize(d)
+            g.check()
+        finally:
+            g.close()
+        twice = np.stack(ring_oracle.ring_mean(starts, lens, list(want))).astype(np.float32)
+        assert bits_equal(np.stack([x.cpu().numpy() for x in xs]), twice), (proto, li)
