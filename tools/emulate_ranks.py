@@ -31,6 +31,7 @@ ap.add_argument("--workload", default="bert")
 ap.add_argument("--proto", default="push")
 ap.add_argument("--steps", type=int, default=30)
 ap.add_argument("--check", type=int, default=1)
+ap.add_argument("--blend", type=int, default=0, help="config 4: average snapshots into means, fused tau=4 blend")
 args = ap.parse_args()
 
 ng = torch.cuda.device_count()
@@ -44,9 +45,19 @@ for m in range(c):
     g = torch.Generator(device=f"cuda:{devices[m]}").manual_seed(20241018 * 1000 + m)
     xs.append(torch.randn(total, device=f"cuda:{devices[m]}", generator=g) * 0.02)
 grp = LoopbackGroup(starts, lens, total, c, torch.float32, protocol=args.proto, devices=devices, timeout_s=20.0)
-grp.bind_tensors(xs)
+means = lives = None
+if args.blend:
+    means = [torch.empty_like(x) for x in xs]
+    lives = []
+    for m, x in enumerate(xs):  # live = snap - 1e-3 * (4 stale N(0,1) updates)
+        g = torch.Generator(device=x.device).manual_seed(7919 + m)
+        lives.append(x - 1e-3 * torch.randn(total, device=x.device, generator=g) * 2.0)
+    grp.bind_tensors(xs, means)
+    grp.bind_live(lives)
+else:
+    grp.bind_tensors(xs)
 ok = None
-if args.check:
+if args.check and not args.blend:
     rows = [x.cpu().numpy() for x in xs]
     want = np.empty_like(rows[0])
     c_oracle.ring_mean_into(c_oracle.MODE_F32_ACC64, starts, lens, rows, None, [want] * c,
@@ -81,6 +92,7 @@ for m in range(c):
     per_gpu[devices[m]] = per_gpu.get(devices[m], 0) + 2 * remote * S / c
 link = max(per_gpu.values())
 print(json.dumps({"ranks": c, "gpus": ng, "ranks_per_gpu": c // ng, "workload": args.workload, "proto": args.proto,
+                  "blend": bool(args.blend),
                   "bitwise_vs_oracle": ok, "ms_per_cycle_median": round(ms, 4), "ms_min": round(min(times), 4),
                   "link_bytes_per_gpu_per_direction": int(link),
                   "link_gbps_per_gpu": round(link / (ms * 1e-3) / 1e9, 1),
