@@ -54,6 +54,23 @@ __device__ __forceinline__ T blend_one(T mean, T live, T snap) {
   return lb == sb ? mean : mean + (live - snap);
 }
 
+// The push transport's fused blend of another owner's chunk runs in two
+// halves: the scatter item that sends this rank's copy of the chunk also
+// turns live into delta(live, snap) (it has the snapshot in hand, and HBM is
+// mostly idle while NVLink carries the scatter), and once the owner's means
+// land the blend item finishes live <- mean + live.  delta() stores -0.0
+// where live and snap are the same bits, and mean + (-0.0) == mean for every
+// mean (RN mode, -0.0 included), so the halves are bit for bit
+// blend_one(mean, live, snap): one IEEE subtract and one IEEE add.
+template <typename T>
+__device__ __forceinline__ T blend_delta(T live, T snap) {
+  using U = typename std::conditional<sizeof(T) == 8, unsigned long long, unsigned>::type;
+  U lb, sb;
+  memcpy(&lb, &live, sizeof(T));
+  memcpy(&sb, &snap, sizeof(T));
+  return lb == sb ? (T)-0.0 : live - snap;
+}
+
 // Fold of one element (chunk edges, misaligned buffers): ring order from s.k.
 // Push with the fused blend: the owner (s.k == me) also blends its own live
 // value, its snapshot being the first member folded.

@@ -125,8 +125,12 @@ __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
 }
 
 // Push with the fused blend: unit u of owner q, once q's mean-delivered flag
-// for it is set: live <- mean + (live - snap) over the unit's range of this
-// rank's buffers.  False when the cycle failed (block must stop).
+// for it is set: live <- mean + live over the unit's range of this rank's
+// buffers, live holding delta(live, snap) since this rank's scatter item of
+// the unit (blend_delta).  That write is ordered before the scatter flag's
+// release, the owner's fold acquires it before releasing the mean-delivered
+// flag this item acquires: causality carries it here.  False when the cycle
+// failed (block must stop).
 template <typename T, int VB>
 __device__ bool blend_item(const CycleParams &p, int q, int64_t u, unsigned long long epoch, unsigned long long t0,
                            int *s_ok) {
@@ -146,23 +150,21 @@ __device__ bool blend_item(const CycleParams &p, int q, int64_t u, unsigned long
   const int64_t nvec = (s.body_hi - s.body_lo) / N;
   const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
   const T *mean = static_cast<const T *>(p.dst[me]);
-  const T *snap = static_cast<const T *>(p.src[me]);
   T *live = static_cast<T *>(p.live_me);
   for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
     const int64_t i = s.body_lo + j * N;
-    Lanes<T, VB> m, l, sn;
+    Lanes<T, VB> m, l;
     m.raw = __ldcg(reinterpret_cast<const Raw *>(mean + i));
-    sn.raw = __ldcs(reinterpret_cast<const Raw *>(snap + i));
-    l.raw = *reinterpret_cast<const Raw *>(live + i);
+    l.raw = __ldcs(reinterpret_cast<const Raw *>(live + i));
 #pragma unroll
-    for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(m.v[e], l.v[e], sn.v[e]);
-    *reinterpret_cast<Raw *>(live + i) = l.raw;
+    for (int e = 0; e < N; ++e) l.v[e] = m.v[e] + l.v[e];
+    __stcs(reinterpret_cast<Raw *>(live + i), l.raw);
   }
   if (uu == 0) {
     const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
     if ((int64_t)threadIdx.x < nhead + ntail) {
       const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x : s.body_hi + ((int64_t)threadIdx.x - nhead);
-      live[i] = blend_one<T>(__ldcg(mean + i), live[i], snap[i]);
+      live[i] = __ldcg(mean + i) + live[i];
     }
   }
   return true;
@@ -235,12 +237,27 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
 #pragma unroll
         for (int c = 0; c < KC; ++c) {
           const int64_t j = j0 + (int64_t)c * kThreads;
-          if (j < jend) v[c] = __ldcs(reinterpret_cast<const Raw *>(src + s.body_lo + j * N));
+          if (j < jend) v[c] = fused ? __ldcg(reinterpret_cast<const Raw *>(src + s.body_lo + j * N))
+                                     : __ldcs(reinterpret_cast<const Raw *>(src + s.body_lo + j * N));
         }
 #pragma unroll
         for (int c = 0; c < KC; ++c) {
           const int64_t j = j0 + (int64_t)c * kThreads;
           if (j < jend) __stcs(reinterpret_cast<Raw *>(stg + s.body_lo + j * N), v[c]);
+        }
+      }
+      if (fused) {
+        // the blend's first half on this rank's copy of the unit (the
+        // snapshot was just read: L2)
+        T *live = static_cast<T *>(p.live_me);
+        for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
+          const int64_t i = s.body_lo + j * N;
+          Lanes<T, VB> l, sn;
+          sn.raw = __ldcs(reinterpret_cast<const Raw *>(src + i));
+          l.raw = *reinterpret_cast<const Raw *>(live + i);
+#pragma unroll
+          for (int e = 0; e < N; ++e) l.v[e] = blend_delta<T>(l.v[e], sn.v[e]);
+          *reinterpret_cast<Raw *>(live + i) = l.raw;
         }
       }
       if (uu == 0) {
@@ -249,6 +266,10 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
           const int64_t i = (int64_t)threadIdx.x < nhead ? s.lo + threadIdx.x
                                                           : s.body_hi + ((int64_t)threadIdx.x - nhead);
           stg[i] = src[i];
+          if (fused) {
+            T *live = static_cast<T *>(p.live_me) + i;
+            *live = blend_delta<T>(*live, src[i]);
+          }
         }
       }
       __threadfence_system();  // this thread's stores, before the unit flag

@@ -51,3 +51,37 @@ def test_every_item_once_and_dependencies_earlier(fused):
             # map on every rank)
             for r in range(C - 1 if fused else 0):
                 assert pos[("f", u)] < pos[("b", u, r)]
+
+
+def test_split_blend_equals_one_pass_blend():
+    """The push kernel's fused blend of another owner's chunk runs in two
+    halves -- live <- delta(live, snap) in the scatter item, live <- mean +
+    live once the owner's means land -- where delta stores -0.0 for
+    bitwise-equal live and snap.  That is bit for bit the one-pass blend
+    mean + (live - snap), exactly mean where live == snap (oracle.blend),
+    signed zeros, infinities and NaN included."""
+    import numpy as np
+
+    from oracle import ring_oracle
+
+    rng = np.random.Generator(np.random.Philox(key=12))
+    for dt in (np.float32, np.float64):
+        n = 1 << 16
+        snap = rng.normal(0, 1, n).astype(dt)
+        live = snap + rng.normal(0, 1e-3, n).astype(dt)
+        mean = rng.normal(0, 1, n).astype(dt)
+        live[::5] = snap[::5]
+        special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, -1e-45, 1.0], dtype=dt)
+        k = len(special)
+        grid = np.array(np.meshgrid(np.arange(k), np.arange(k), np.arange(k))).reshape(3, -1)
+        mean = np.concatenate([mean, special[grid[0]]])
+        live = np.concatenate([live, special[grid[1]]])
+        snap = np.concatenate([snap, special[grid[2]]])
+        ut = {4: np.uint32, 8: np.uint64}[np.dtype(dt).itemsize]
+        with np.errstate(all="ignore"):
+            delta = np.where(live.view(ut) == snap.view(ut), dt(-0.0), live - snap)
+            two_half = mean + delta
+            want = ring_oracle.blend(mean, live, snap)
+        nan = np.isnan(want)
+        assert np.array_equal(np.isnan(two_half), nan)
+        assert np.array_equal(two_half.view(ut)[~nan], want.view(ut)[~nan]), dt
