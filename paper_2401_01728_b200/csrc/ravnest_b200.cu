@@ -333,7 +333,8 @@ int build_tables(rv_plan *p) {
   } else {
     p->kernel = pick_kernel(mode, cb, vec, push, &U);
     p->block_threads = kThreads;
-    p->smem_bytes = 0;
+    // the fused push blend streams its operands through shared memory
+    p->smem_bytes = p->fused_blend ? (size_t)kBlendSmem : 0;
     tile_vecs = (int64_t)kThreads * U;
   }
   RV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->occ, p->kernel, p->block_threads, p->smem_bytes));

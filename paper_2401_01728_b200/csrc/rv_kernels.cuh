@@ -124,6 +124,67 @@ __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
   return segs[a];
 }
 
+// The fused blend's passes stream two operands per vector through shared
+// memory with cp.async (LDGSTS): kBlendStages vectors per thread in flight
+// and almost no registers, where a register loop kept one (a blend item is
+// local HBM work and was latency-bound at one vector per thread).  Each
+// thread reads back only the slots it filled itself, so waiting on its own
+// cp.async groups is enough (no block barrier).
+constexpr int kBlendStages = 4;
+constexpr int kBlendSmem = kBlendStages * 2 * kThreads * 16;  // dynamic shared memory of a fused push launch
+
+template <int VB>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? VB : 0;  // src-size 0: no global read, nothing to wait for
+  if constexpr (VB == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(sa), "l"(gmem), "n"(VB), "r"(n)
+                 : "memory");
+}
+
+// live[j] <- f(a[j], live[j]) for vectors j in [jbeg, jend) of a chunk body
+// (pointers already at the body start); ADD: f = a + live (second half, a =
+// mean), else f = delta(live, a) (first half, a = snapshot).
+template <typename T, int VB, bool ADD>
+__device__ __forceinline__ void blend_stream(const T *a, T *live, int64_t jbeg, int64_t jend) {
+  constexpr int N = VB / sizeof(T);
+  using Raw = typename RawVec<VB>::type;
+  extern __shared__ __align__(128) unsigned char smem[];  // kBlendSmem bytes (fused push launches only)
+  Raw(*s_buf)[2][kThreads] = reinterpret_cast<Raw(*)[2][kThreads]>(smem);
+  const int tid = threadIdx.x;
+  const int64_t first = jbeg + tid;
+  // prologue: stages 0 .. S-2
+#pragma unroll
+  for (int k = 0; k < kBlendStages - 1; ++k) {
+    const int64_t j = first + (int64_t)k * kThreads;
+    const bool ok = j < jend;
+    cp_async<VB>(&s_buf[k][0][tid], a + (ok ? j : jbeg) * N, ok);
+    cp_async<VB>(&s_buf[k][1][tid], live + (ok ? j : jbeg) * N, ok);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int st = 0;
+  for (int64_t j = first; j < jend; j += kThreads) {
+    // issue the vector S-1 iterations ahead into the stage freed last round
+    const int64_t jn = j + (int64_t)(kBlendStages - 1) * kThreads;
+    const int sn = st == 0 ? kBlendStages - 1 : st - 1;
+    const bool ok = jn < jend;
+    cp_async<VB>(&s_buf[sn][0][tid], a + (ok ? jn : jbeg) * N, ok);
+    cp_async<VB>(&s_buf[sn][1][tid], live + (ok ? jn : jbeg) * N, ok);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kBlendStages - 1) : "memory");
+    Lanes<T, VB> x, l;
+    x.raw = s_buf[st][0][tid];
+    l.raw = s_buf[st][1][tid];
+#pragma unroll
+    for (int e = 0; e < N; ++e) l.v[e] = ADD ? x.v[e] + l.v[e] : blend_delta<T>(l.v[e], x.v[e]);
+    __stcs(reinterpret_cast<Raw *>(live + j * N), l.raw);
+    st = st + 1 == kBlendStages ? 0 : st + 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // Push with the fused blend: unit u of owner q, once q's mean-delivered flag
 // for it is set: live <- mean + live over the unit's range of this rank's
 // buffers, live holding delta(live, snap) since this rank's scatter item of
@@ -151,15 +212,7 @@ __device__ bool blend_item(const CycleParams &p, int q, int64_t u, unsigned long
   const int64_t jbeg = uu * p.unit_vecs, jend = min(nvec, jbeg + p.unit_vecs);
   const T *mean = static_cast<const T *>(p.dst[me]);
   T *live = static_cast<T *>(p.live_me);
-  for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
-    const int64_t i = s.body_lo + j * N;
-    Lanes<T, VB> m, l;
-    m.raw = __ldcg(reinterpret_cast<const Raw *>(mean + i));
-    l.raw = __ldcs(reinterpret_cast<const Raw *>(live + i));
-#pragma unroll
-    for (int e = 0; e < N; ++e) l.v[e] = m.v[e] + l.v[e];
-    __stcs(reinterpret_cast<Raw *>(live + i), l.raw);
-  }
+  blend_stream<T, VB, true>(mean + s.body_lo, live + s.body_lo, jbeg, jend);
   if (uu == 0) {
     const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
     if ((int64_t)threadIdx.x < nhead + ntail) {
@@ -250,15 +303,7 @@ ring_push_kernel(const __grid_constant__ CycleParams p) {
         // the blend's first half on this rank's copy of the unit (the
         // snapshot was just read: L2)
         T *live = static_cast<T *>(p.live_me);
-        for (int64_t j = jbeg + threadIdx.x; j < jend; j += kThreads) {
-          const int64_t i = s.body_lo + j * N;
-          Lanes<T, VB> l, sn;
-          sn.raw = __ldcs(reinterpret_cast<const Raw *>(src + i));
-          l.raw = *reinterpret_cast<const Raw *>(live + i);
-#pragma unroll
-          for (int e = 0; e < N; ++e) l.v[e] = blend_delta<T>(l.v[e], sn.v[e]);
-          *reinterpret_cast<Raw *>(live + i) = l.raw;
-        }
+        blend_stream<T, VB, false>(src + s.body_lo, live + s.body_lo, jbeg, jend);
       }
       if (uu == 0) {
         const int64_t nhead = s.body_lo - s.lo, ntail = s.hi - s.body_hi;
