@@ -25,6 +25,23 @@ union Lanes {
   T v[VB / sizeof(T)];
 };
 
+// Fused push blend: its passes stream operands through shared memory with
+// cp.async (see blend_stream, rv_kernels.cuh); the fold also prefetches the
+// owner's live vectors this way.
+constexpr int kBlendStages = 4;
+constexpr int kBlendSmem = kBlendStages * 2 * 256 * 16;  // dynamic shared memory of a fused push launch
+
+template <int VB>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? VB : 0;  // src-size 0: no global read, nothing to wait for
+  if constexpr (VB == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(sa), "l"(gmem), "n"(VB), "r"(n)
+                 : "memory");
+}
+
 template <typename T, typename Acc>
 __device__ __forceinline__ T finish(Acc acc, const CycleParams &p) {
   // IEEE true division by C (multiring.py:219).  For C a power of two the
@@ -98,7 +115,24 @@ template <typename T, typename Acc, int CB, int VB, int U, bool PUSH>
 __device__ __forceinline__ void fold_pass(const CycleParams &p, const Seg &s, int64_t j0, int64_t jend) {
   constexpr int N = VB / sizeof(T);
   using Raw = typename RawVec<VB>::type;
+  static_assert(U * 16 * 256 <= kBlendSmem, "live prefetch slots exceed the fused launch's shared memory");
   Lanes<T, VB> x[U][CB];
+  extern __shared__ __align__(128) unsigned char smem[];  // fused push launches only (kBlendSmem)
+  Raw *lbuf = reinterpret_cast<Raw *>(smem);               // [U][kThreads]: this thread's live prefetch
+  // (not for fp64 storage at CB >= 8, whose address registers would spill)
+  constexpr bool kPrefetch = PUSH && (sizeof(T) == 4 || CB <= 4);
+  if (kPrefetch && p.live_me) {
+    // the fused blend of the owner's own copy needs its live vectors after
+    // the fold: fetch them now, alongside the members, without registers
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + (int64_t)u * kThreads;
+      const bool ok = j < jend;
+      cp_async<VB>(&lbuf[u * kThreads + threadIdx.x],
+                   static_cast<const T *>(p.live_me) + s.body_lo + (ok ? j : j0) * N, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t j = j0 + (int64_t)u * kThreads;
@@ -132,12 +166,16 @@ __device__ __forceinline__ void fold_pass(const CycleParams &p, const Seg &s, in
       for (int q = 0; q < CB; ++q)
         if (q < p.C) __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.dst[q]) + i), out.raw);
       if (PUSH && p.live_me) {  // fused blend of the owner's own copy (x[u][0] is its snapshot)
-        Raw *lp = reinterpret_cast<Raw *>(static_cast<T *>(p.live_me) + i);
         Lanes<T, VB> l;
-        l.raw = *lp;
+        if constexpr (kPrefetch) {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+          l.raw = lbuf[u * kThreads + threadIdx.x];
+        } else {
+          l.raw = *reinterpret_cast<const Raw *>(static_cast<const T *>(p.live_me) + i);
+        }
 #pragma unroll
         for (int e = 0; e < N; ++e) l.v[e] = blend_one<T>(out.v[e], l.v[e], x[u][0].v[e]);
-        *lp = l.raw;
+        __stcs(reinterpret_cast<Raw *>(static_cast<T *>(p.live_me) + i), l.raw);
       }
     }
   }

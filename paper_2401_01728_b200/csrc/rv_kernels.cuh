@@ -130,20 +130,6 @@ __device__ __forceinline__ Seg find_unit(const Seg *segs, int nseg, int64_t u) {
 // local HBM work and was latency-bound at one vector per thread).  Each
 // thread reads back only the slots it filled itself, so waiting on its own
 // cp.async groups is enough (no block barrier).
-constexpr int kBlendStages = 4;
-constexpr int kBlendSmem = kBlendStages * 2 * kThreads * 16;  // dynamic shared memory of a fused push launch
-
-template <int VB>
-__device__ __forceinline__ void cp_async(void *smem, const void *gmem, bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = pred ? VB : 0;  // src-size 0: no global read, nothing to wait for
-  if constexpr (VB == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(sa), "l"(gmem), "n"(VB), "r"(n)
-                 : "memory");
-}
-
 // live[j] <- f(a[j], live[j]) for vectors j in [jbeg, jend) of a chunk body
 // (pointers already at the body start); ADD: f = a + live (second half, a =
 // mean), else f = delta(live, a) (first half, a = snapshot).
