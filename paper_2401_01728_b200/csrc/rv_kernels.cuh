@@ -393,14 +393,6 @@ __device__ __forceinline__ bool ll_load(const CycleParams &p, const unsigned *ad
   return true;
 }
 
-// One look at an LL word pair (no polling): {v0, e0, v1, e1}.
-__device__ __forceinline__ uint4 ll_peek(const unsigned *addr) {
-  uint4 r;
-  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(addr) : "memory");
-  return r;
-}
-
 template <typename Acc, int CB>
 __global__ void __launch_bounds__(kThreads, 2)
 ring_ll_kernel(const __grid_constant__ CycleParams p) {
@@ -459,17 +451,6 @@ ring_ll_kernel(const __grid_constant__ CycleParams p) {
       const bool two = i0 + 1 < s.hi;
       const int64_t word = s.stage_off + (i0 - s.lo);
       const unsigned *stage = static_cast<const unsigned *>(p.stage[me]);
-      // peek at every member's word pair at once (C - 1 loads in flight
-      // instead of one round trip per member); only words that have not
-      // landed yet are polled below
-      uint4 peek[CB];
-#pragma unroll
-      for (int j = 1; j < CB; ++j) {
-        if (j < C) {
-          const int mm = me + j < C ? me + j : me + j - C;
-          peek[j] = ll_peek(stage + 2 * ((int64_t)mm * p.stride + word));
-        }
-      }
       Acc a0 = 0, a1 = 0;
       int m = s.k;  // == me: the fold starts at the owner
 #pragma unroll
@@ -479,9 +460,6 @@ ring_ll_kernel(const __grid_constant__ CycleParams p) {
           if (m == me) {
             v0 = src[i0];
             v1 = two ? src[i0 + 1] : 0.f;
-          } else if (peek[j].y == e && peek[j].w == e) {
-            v0 = __uint_as_float(peek[j].x);
-            v1 = __uint_as_float(peek[j].z);
           } else {
             const unsigned diag = (2u << 16) | ((unsigned)p.lane << 8) | (unsigned)m;
             if (!ll_load(p, stage + 2 * ((int64_t)m * p.stride + word), e, &v0, &v1, diag)) {

@@ -1,5 +1,5 @@
 #!/bin/bash
-# LL fold: peek at every member's word pair at once (llpeek) vs one polled
+# (Round 2, not kept: no change.) LL fold: peek at every member's word pair at once (llpeek) vs one polled
 # load per member in turn (llseq): LL parity tests, then the small-shard
 # sweep points at the box's GPU count, alternating.
 set -u
