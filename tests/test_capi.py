@@ -94,3 +94,15 @@ def test_lane_partition(lens, n_lanes):
             if hi > lo:
                 r = max(i for i, s in enumerate(starts) if s <= lo)
                 assert hi <= starts[r] + lens[r]
+
+
+def test_plan_option_ids_match_the_header():
+    """rv_plan_set_option's RV_OPT_* ids in the header are the ones the
+    Python plans pass (kernel choice comes only from these, never from the
+    environment)."""
+    with open(os.path.join(ROOT, "include", "ravnest_b200.h")) as f:
+        defs = dict((k, int(v)) for k, v in re.findall(r"^#define (RV_OPT_\w+) (\d+)", f.read(), re.M))
+    assert defs == {f"RV_OPT_{k.upper()}": v for k, v in _native.OPTIONS.items()}
+    src = open(os.path.join(ROOT, "paper_2401_01728_b200", "csrc", "ravnest_b200.cu")).read()
+    src += open(os.path.join(ROOT, "paper_2401_01728_b200", "csrc", "rv_dispatch.cuh")).read()
+    assert "getenv" not in src
