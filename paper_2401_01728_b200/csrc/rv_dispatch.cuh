@@ -69,6 +69,19 @@ KernelFn pick_cb(int c, bool push, int *u_out) {
 #endif
 constexpr int kTmaStages = RV_TMA_STAGES;
 constexpr int kTmaStageBytes = RV_TMA_STAGE_KB * 1024;
+// The fused-blend kernel (each stage carries C snapshot and C live tiles):
+// 3 stages of 48 KB.  GPT-2 C=8 config 4, alternating A/B builds
+// (profiles/r02/ab_tma_blend_layouts_n1.txt): 3 x 48 KB 0.987 of HBM on the
+// 4*C*S basis, 2 x 64 KB 0.915, 2 x 72 KB 0.943 (and too much shared
+// memory at C <= 4), 3 x 40 KB 0.827.
+#ifndef RV_TMA_BL_STAGES  // A/B builds only override these
+#define RV_TMA_BL_STAGES 3
+#endif
+#ifndef RV_TMA_BL_STAGE_KB
+#define RV_TMA_BL_STAGE_KB 48
+#endif
+constexpr int kTmaBlStages = RV_TMA_BL_STAGES;
+constexpr int kTmaBlStageBytes = RV_TMA_BL_STAGE_KB * 1024;
 
 // BL: the fused-blend kernel; a stage carries C src and C live tiles, so the
 // same stage bytes hold half the vectors per member.
@@ -94,9 +107,9 @@ KernelFn pick_tma(int c, int *tv_out) {
 KernelFn pick_tma_kernel(int mode, int c, bool blend, int *tv_out, size_t *smem_out) {
   KernelFn k;
   if (blend)
-    k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes, true>(c, tv_out)
-      : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes, true>(c, tv_out)
-                           : pick_tma<double, double, kTmaStages, kTmaStageBytes, true>(c, tv_out);
+    k = mode == kF32Acc64 ? pick_tma<float, double, kTmaBlStages, kTmaBlStageBytes, true>(c, tv_out)
+      : mode == kF32Native ? pick_tma<float, float, kTmaBlStages, kTmaBlStageBytes, true>(c, tv_out)
+                           : pick_tma<double, double, kTmaBlStages, kTmaBlStageBytes, true>(c, tv_out);
   else
     k = mode == kF32Acc64 ? pick_tma<float, double, kTmaStages, kTmaStageBytes>(c, tv_out)
       : mode == kF32Native ? pick_tma<float, float, kTmaStages, kTmaStageBytes>(c, tv_out)
@@ -104,7 +117,7 @@ KernelFn pick_tma_kernel(int mode, int c, bool blend, int *tv_out, size_t *smem_
   const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
   // input stages, then the output buffers: 3 mean tiles, or (blend) 2 x
   // (mean + C live tiles) -- must match ring_tma_kernel's NOB / OUTS
-  *smem_out = blend ? (size_t)kTmaStages * 2 * cb * (*tv_out) * 16 + 2 * (size_t)(cb + 1) * (*tv_out) * 16
+  *smem_out = blend ? (size_t)kTmaBlStages * 2 * cb * (*tv_out) * 16 + 2 * (size_t)(cb + 1) * (*tv_out) * 16
                     : (size_t)kTmaStages * cb * (*tv_out) * 16 + 3 * (size_t)(*tv_out) * 16;
   return k;
 }
