@@ -12,9 +12,11 @@ with alpha the fixed cost (launch + arrive/depart barriers) and beta the
 sustained per-GPU, per-direction NVLink rate of the transport.  ``fit``
 calibrates (alpha, beta) by least squares on relative error from sweep rows
 (tools/sweep.py output); ``CALIBRATED`` holds the values fitted on
-profiles/r01/sweep_n4_current.jsonl (4 x B200, 24 shard-size x ring-count
-points from 1 MiB to 8 GiB per cluster; max relative error 8 % for pull,
-16 % for push, under 4 % above 32 MiB per cluster).
+profiles/r02/sweep_r02_n4.jsonl (4 x B200, round-2 kernels, 24 shard-size x
+ring-count points from 1 MiB to 8 GiB per cluster; max relative error 4 % for
+pull, 15 % for push, 3 % for LL, under 2.1 % above 32 MiB per cluster).  At
+2 GPUs the same fit gives pull 18.3 us / 676.5 GB/s, push 26.6 us / 697.6
+GB/s (profiles/r02/sweep_r02_n2.jsonl).
 """
 
 from __future__ import annotations
@@ -35,9 +37,9 @@ class NvlinkModel:
 
 
 CALIBRATED = {
-    "pull": NvlinkModel(27.82e-6, 642.0e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs)"),
-    "push": NvlinkModel(30.77e-6, 677.4e9, "profiles/r01/sweep_n4_current.jsonl (4 GPUs, adaptive units)"),
-    "ll": NvlinkModel(10.09e-6, 297.4e9, "profiles/r01/sweep_n4_small_ll.jsonl (4 GPUs, <= 4 MiB per cluster)"),
+    "pull": NvlinkModel(26.25e-6, 652.1e9, "profiles/r02/sweep_r02_n4.jsonl (4 GPUs)"),
+    "push": NvlinkModel(31.30e-6, 689.3e9, "profiles/r02/sweep_r02_n4.jsonl (4 GPUs, adaptive units)"),
+    "ll": NvlinkModel(10.42e-6, 298.2e9, "profiles/r02/sweep_r02_n4.jsonl (4 GPUs, <= 16 MiB per cluster)"),
     "nccl": NvlinkModel(3.16e-6, 606.2e9, "profiles/r01/sweep_n4.jsonl; + 23.3 us per ring call"),
 }
 

@@ -10,7 +10,7 @@ import paper_2401_01728_b200 as rv
 from paper_2401_01728_b200 import cli, cost
 from conftest import ROOT, GOLDEN
 
-SWEEP = os.path.join(ROOT, "profiles", "r01", "sweep_n4_current.jsonl")
+SWEEP = os.path.join(ROOT, "profiles", "r02", "sweep_r02_n4.jsonl")
 
 
 def rows():
@@ -19,7 +19,7 @@ def rows():
 
 
 def test_models_fit_measured_sweep():
-    for proto, tol in (("pull", 0.10), ("push", 0.18)):
+    for proto, tol in (("pull", 0.06), ("push", 0.18)):
         model, err = cost.fit(rows(), proto)
         assert err < tol, proto
         assert 600e9 < model.beta_Bps < 720e9
