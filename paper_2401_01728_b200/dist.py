@@ -44,19 +44,26 @@ def _close(device: int, ptr: int) -> None:
     N.load().rv_ipc_close(int(device), ctypes.c_void_p(int(ptr)))
 
 
-PUSH_MIN_BYTES = 32 << 20
+PUSH_MIN_BYTES = 32 << 20       # 3 or more ranks
+PUSH_MIN_BYTES_C2 = 192 << 20   # 2 ranks
 LL_MAX_BYTES = 4 << 20
 
 
-def choose_protocol(protocol: str, bytes_per_cluster: int, fp32: bool = True) -> str:
+def choose_protocol(protocol: str, bytes_per_cluster: int, fp32: bool = True, n_ranks: int | None = None) -> str:
     """'auto': the LL transport for fp32 sets up to 4 MiB per cluster
     (latency-bound: no fences or barriers), store-only push from 32 MiB (its
-    per-unit flags pay off and NVLink stores outrun loads), pull in between.
-    Depends only on the schedule and dtype, so every rank picks the same."""
+    per-unit flags pay off and NVLink stores outrun loads) -- from 192 MiB
+    with 2 ranks, where pull stays ahead longer -- and pull in between.
+    Round-2 sweep (profiles/r02/sweep_r02_n{2,4}.jsonl): at 4 GPUs push
+    leads from 32 MiB; at 2 GPUs pull leads up to 128 MiB (ResNet-50, 102 MB:
+    pull 552.7 vs push 546 GB/s; BERT, 438 MB: push 671 vs pull 647,
+    profiles/r02/proto_crossover_n2.txt).  Depends only on the schedule,
+    dtype and rank count, so every rank picks the same."""
     if protocol == "auto":
         if fp32 and bytes_per_cluster <= LL_MAX_BYTES:
             return "ll"
-        return "push" if bytes_per_cluster >= PUSH_MIN_BYTES else "pull"
+        push_min = PUSH_MIN_BYTES_C2 if n_ranks == 2 else PUSH_MIN_BYTES
+        return "push" if bytes_per_cluster >= push_min else "pull"
     if protocol not in ("pull", "push", "ll"):
         raise ConfigError(f"unknown protocol {protocol!r} (auto, pull, push or ll)")
     return protocol
@@ -169,7 +176,7 @@ class DistRingGroup:
             self.plan.set_timeout(timeout_s)
         if max_blocks:
             self.plan.set_max_blocks(max_blocks)
-        protocol = choose_protocol(protocol, total * src.element_size(), src.element_size() == 4)
+        protocol = choose_protocol(protocol, total * src.element_size(), src.element_size() == 4, self.world)
         self.protocol = protocol
         self.plan.set_protocol(protocol)
         flag_ptr, _ = self.plan.flag_area()

@@ -108,3 +108,21 @@ def test_collective_agreement_raises_on_every_rank(case, want):
     assert [o[1] for o in out] == [want, want], out
     if want == "LayoutError":
         assert all("rank 1" in o[2] for o in out)
+
+
+def test_auto_protocol_thresholds():
+    """'auto' transport choice (dist.choose_protocol): a function of the
+    bytes per cluster, dtype and rank count only, so every rank agrees."""
+    from paper_2401_01728_b200.dist import choose_protocol
+
+    mib = 1 << 20
+    assert choose_protocol("auto", 4 * mib) == "ll"
+    assert choose_protocol("auto", 4 * mib, fp32=False) == "pull"
+    assert choose_protocol("auto", 16 * mib, n_ranks=4) == "pull"
+    assert choose_protocol("auto", 32 * mib, n_ranks=4) == "push"
+    assert choose_protocol("auto", 102 * mib, n_ranks=2) == "pull"   # ResNet-50 at 2 GPUs
+    assert choose_protocol("auto", 438 * mib, n_ranks=2) == "push"   # BERT-base at 2 GPUs
+    assert choose_protocol("auto", 102 * mib, n_ranks=8) == "push"
+    assert choose_protocol("pull", 1 << 30) == "pull"
+    with pytest.raises(Exception):
+        choose_protocol("nvls", 1)
