@@ -119,3 +119,33 @@ def test_drain_controller_is_asynchronous():
     for cid in range(c):
         assert bits_equal(working[cid], want[cid]), cid
     del ravnest
+
+
+def test_numpy_dropin_input_forms():
+    """apply_ring_mean's numpy path takes what the reference's np.array(x,
+    dtype=float64) takes (multiring.py:309): float32 or float64 arrays,
+    strided views, lists; returns new float64 arrays bitwise the reference;
+    inputs untouched; one cluster returns float64 copies."""
+    ravnest = import_reference("ravnest")
+    from ravnest import multiring as ref_mr
+
+    lay = {cid: [ref_mr.ParamRange(0, 700), ref_mr.ParamRange(700, 301)] for cid in (3, 1, 7)}
+    sched = ref_mr.build_ring_schedule(lay)
+    rng = np.random.Generator(np.random.Philox(key=21))
+    base = {cid: rng.normal(0, 1, 2 * 1001) for cid in lay}
+    forms = {
+        3: base[3][::2].astype(np.float32),   # float32, strided
+        1: base[1][:1001].copy(),             # float64
+        7: list(base[7][1001:]),              # a list
+    }
+    keep = {c: np.array(v, copy=True) for c, v in forms.items()}
+    want = ref_mr.apply_ring_mean(sched, forms)
+    got = mr.apply_ring_mean(sched, forms)
+    assert sorted(got) == sorted(want)
+    for c in lay:
+        assert got[c].dtype == np.float64 and got[c].shape == (1001,)
+        assert bits_equal(got[c], want[c]), c
+        assert bits_equal(np.asarray(forms[c], dtype=keep[c].dtype), keep[c])  # inputs untouched
+    one = mr.apply_ring_mean(sched, {3: forms[3]})
+    assert one[3].dtype == np.float64 and bits_equal(one[3], forms[3].astype(np.float64))
+    del ravnest
