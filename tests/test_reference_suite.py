@@ -33,7 +33,7 @@ FILES = ["test_multiring.py", "test_orchestrator.py", "test_oracle.py", "test_cl
 KNOWN_REFERENCE_FAILURE = "test_six_random"  # test_oracle.py::TestMeanReference
 
 
-def run_reference_suite(tmp_path, oracle_cycle: bool):
+def run_reference_suite(tmp_path, oracle_cycle: bool, files=FILES):
     tests = ref_tests()
     if tests is None or not os.path.isdir(os.path.join(REFERENCE_INSTALL, "ravnest")):
         pytest.skip("needs the reference's tests and baseline/_ref")
@@ -41,7 +41,7 @@ def run_reference_suite(tmp_path, oracle_cycle: bool):
                PYTHONPATH=os.pathsep.join([REFERENCE_INSTALL, os.path.join(ROOT, "tests"), ROOT]))
     cmd = [sys.executable, "-m", "pytest", "-p", "ref_suite_plugin", "-p", "no:cacheprovider", "-q",
            "-k", f"not {KNOWN_REFERENCE_FAILURE}"]
-    cmd += [os.path.join(tests, f) for f in FILES]
+    cmd += [os.path.join(tests, f) for f in files]
     res = subprocess.run(cmd, cwd=tmp_path, env=env, capture_output=True, text=True, timeout=900)
     tail = res.stdout[-3000:] + res.stderr[-2000:]
     assert res.returncode == 0, tail
@@ -59,9 +59,11 @@ def test_reference_averaging_tests_pass_through_the_drop_in(tmp_path):
 
 @pytest.mark.gpu
 def test_reference_averaging_tests_pass_on_the_gpu(tmp_path):
-    """The same reference test files with every averaging cycle on the GPU
+    """The same reference test files, plus its acceptance suite
+    (test_acceptance.py: criterion 1's 1000 random instances, the training
+    criteria, the cost model), with every averaging cycle on the GPU
     (float64 kernel, bitwise the reference)."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    run_reference_suite(tmp_path, oracle_cycle=False)
+    run_reference_suite(tmp_path, oracle_cycle=False, files=FILES + ["test_acceptance.py"])
