@@ -117,7 +117,8 @@ KernelFn pick_tma_kernel(int mode, int c, bool blend, int *tv_out, size_t *smem_
   const int cb = c <= 2 ? 2 : c <= 4 ? 4 : c <= 8 ? 8 : 16;
   // input stages, then the output buffers: 3 mean tiles, or (blend) 2 x
   // (mean + C live tiles) -- must match ring_tma_kernel's NOB / OUTS
-  *smem_out = blend ? (size_t)kTmaBlStages * 2 * cb * (*tv_out) * 16 + 2 * (size_t)(cb + 1) * (*tv_out) * 16
+  *smem_out = blend ? (size_t)kTmaBlStages * 2 * cb * (*tv_out) * 16 +
+                           (size_t)tma_out_buffers(true, cb) * (cb + 1) * (*tv_out) * 16
                     : (size_t)kTmaStages * cb * (*tv_out) * 16 + 3 * (size_t)(*tv_out) * 16;
   return k;
 }

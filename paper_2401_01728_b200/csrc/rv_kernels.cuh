@@ -553,6 +553,19 @@ __device__ __forceinline__ void bulk_store(void *gmem, const void *smem, unsigne
                : "memory");
 }
 
+// Output buffers of the TMA kernel (bulk-store groups in flight): 3 for the
+// plain kernel; the fused-blend kernel's output tiles are C + 1 times larger,
+// so 2.  Three where shared memory allows (CB >= 8, RV_TMA_BL_NOB3 A/B
+// builds) measured the same: GPT-2 / BERT C=8 config 4 0.955-0.958 vs
+// 0.952-0.963 of HBM (profiles/r02/ab_tma_blend_nob_n1.txt).
+__host__ __device__ constexpr int tma_out_buffers(bool bl, int cb) {
+#ifdef RV_TMA_BL_NOB3
+  return bl ? (cb >= 8 ? 3 : 2) : 3;
+#else
+  return bl ? 2 : 3;
+#endif
+}
+
 // BL (fused delayed-update blend): each stage also carries every member's
 // live tile; the consumers write the mean tile and C blended live tiles,
 // which go out by bulk store to dst and live.
@@ -562,7 +575,7 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = 16 / sizeof(T);
   constexpr int SLOTS = BL ? 2 * CB : CB;  // tiles per stage: src (ring order), then live
   constexpr int OUTS = BL ? CB + 1 : 1;    // output tiles: mean, then blended live
-  constexpr int NOB = BL ? 2 : 3;          // output buffers (bulk-store groups in flight)
+  constexpr int NOB = tma_out_buffers(BL, CB);  // output buffers (bulk-store groups in flight)
   extern __shared__ __align__(128) unsigned char smem[];
   uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][SLOTS][TV]
   uint4 *out = in + (size_t)STAGES * SLOTS * TV;                       // [NOB][OUTS][TV]
