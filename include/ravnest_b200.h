@@ -202,10 +202,11 @@ int rv_allreduce_mean_host_lanes(rv_plan *plan, int first_lane, int n_lanes, con
 /* Blocking: device-side status of the plan (RV_OK or RV_E_TIMEOUT), and a
  * description of the first stall "(ring=r, phase=..., member=m)". */
 int rv_plan_status(rv_plan *plan, char *diag, size_t diag_len);
-/* Clears the status and re-aligns the lane bookkeeping so this plan can run
- * again.  After a cross-rank stall every rank of the group must reset (or
- * rebuild its plan) before the next cycle; resetting one rank alone leaves
- * the peers' barrier epochs behind. */
+/* Clears the status and re-aligns this plan's own lane bookkeeping (the
+ * arrive bookkeeping with its epoch).  It does not re-synchronise epochs
+ * across ranks: after a cross-rank stall the ranks may have run different
+ * numbers of cycles, so the group must be rebuilt (every rank destroys and
+ * recreates its plan, as DistRingGroup.close() + a new group do). */
 int rv_plan_reset_status(rv_plan *plan);
 int rv_plan_destroy(rv_plan *plan);
 
