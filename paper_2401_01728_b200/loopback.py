@@ -74,28 +74,34 @@ class LoopbackGroup:
                 if a != b:
                     N.check(lib.rv_enable_peer_access(a, b), "rv_enable_peer_access")
         self.plans = []
-        for m in range(self.C):
-            dev = self.devices[m]
-            # every rank's kernels must be resident together: the cycle
-            # kernels run <= 2 blocks per SM (__launch_bounds__(256, 2)), so
-            # 2*SMs / (ranks on the device) blocks per rank leave room for all
-            budget = blocks_per_rank or max(1, 2 * lib.rv_device_sm_count(dev) // self.devices.count(dev))
-            p = DevicePlan(dev, self.C, self.starts, self.lens, self.total, _dtype_code(dtype), acc)
-            p.set_options(options)
-            if self.lanes != 1:
-                p.set_lanes(self.lanes)
-            if timeout_s is not None:
-                p.set_timeout(timeout_s)
-            p.set_max_blocks(budget)
-            p.set_protocol(protocol)
-            self.plans.append(p)
-        flags = [p.flag_area()[0] for p in self.plans]
-        push = [p.push_area()[0] for p in self.plans] if protocol in ("push", "ll") else None
-        for m, p in enumerate(self.plans):
-            p.set_local([m])
-            p.set_peers(m, self.C, flags)
-            if push is not None:
-                p.set_push_peers(push)
+        try:
+            for m in range(self.C):
+                dev = self.devices[m]
+                # every rank's kernels must be resident together: the cycle
+                # kernels run <= 2 blocks per SM (__launch_bounds__(256, 2)),
+                # so 2*SMs / (ranks on the device) blocks per rank leave room
+                budget = blocks_per_rank or max(1, 2 * lib.rv_device_sm_count(dev) // self.devices.count(dev))
+                p = DevicePlan(dev, self.C, self.starts, self.lens, self.total, _dtype_code(dtype), acc)
+                self.plans.append(p)
+                p.set_options(options)
+                if self.lanes != 1:
+                    p.set_lanes(self.lanes)
+                if timeout_s is not None:
+                    p.set_timeout(timeout_s)
+                p.set_max_blocks(budget)
+                p.set_protocol(protocol)
+            flags = [p.flag_area()[0] for p in self.plans]
+            push = [p.push_area()[0] for p in self.plans] if protocol in ("push", "ll") else None
+            for m, p in enumerate(self.plans):
+                p.set_local([m])
+                p.set_peers(m, self.C, flags)
+                if push is not None:
+                    p.set_push_peers(push)
+        except BaseException:
+            for p in self.plans:  # no half-built group keeps device memory
+                p.close()
+            self.plans = []
+            raise
         import torch
 
         # one stream per rank (torch's pool holds 32 per device: more would alias)
