@@ -514,7 +514,10 @@ ring_ll_kernel(const __grid_constant__ CycleParams p) {
 // C bulk stores (shared->global) of it, double-buffered.  No register
 // staging of loads, so each SM keeps STAGES * C * TV * 16 bytes in flight.
 
-constexpr int kTmaConsumers = 256;
+#ifndef RV_TMA_CONSUMERS  // A/B builds only
+#define RV_TMA_CONSUMERS 256
+#endif
+constexpr int kTmaConsumers = RV_TMA_CONSUMERS;
 
 __device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -570,7 +573,7 @@ __host__ __device__ constexpr int tma_out_buffers(bool bl, int cb) {
 // live tile; the consumers write the mean tile and C blended live tiles,
 // which go out by bulk store to dst and live.
 template <typename T, typename Acc, int CB, int TV, int STAGES, bool BL = false>
-__global__ void __launch_bounds__(kTmaConsumers + 32, 2)
+__global__ void __launch_bounds__(kTmaConsumers + 32, kTmaConsumers > 256 ? 1 : 2)
 ring_tma_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = 16 / sizeof(T);
   constexpr int SLOTS = BL ? 2 * CB : CB;  // tiles per stage: src (ring order), then live
