@@ -327,7 +327,7 @@ int build_tables(rv_plan *p) {
     int tv = 0;
     p->fused_blend = p->blend;
     p->kernel = pick_tma_kernel(mode, cb, p->blend, &tv, &p->smem_bytes);
-    p->block_threads = kTmaConsumers + 32;
+    p->block_threads = tma_consumers(p->blend) + 32;
     RV_CUDA(cudaFuncSetAttribute(p->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem_bytes));
     tile_vecs = tv;
   } else {

@@ -509,15 +509,26 @@ ring_ll_kernel(const __grid_constant__ CycleParams p) {
 // buffers): HBM-bound, so tiles stream through shared memory with bulk async
 // copies.  Warp 0 / lane 0 produces: for each tile it loads the tile of all C
 // members (cp.async.bulk global->shared, completion on a per-stage mbarrier)
-// into a STAGES-deep ring.  Warps 1..8 consume: fold from shared memory in
-// ring order, write the mean tile to shared memory, and one consumer issues
-// C bulk stores (shared->global) of it, double-buffered.  No register
+// into a STAGES-deep ring.  The consumer warps (4; 8 with the fused blend)
+// fold from shared memory in ring order, write the mean tile to shared
+// memory, and one consumer issues C bulk stores (shared->global) of it, from
+// rotating output buffers.  No register
 // staging of loads, so each SM keeps STAGES * C * TV * 16 bytes in flight.
 
-#ifndef RV_TMA_CONSUMERS  // A/B builds only
-#define RV_TMA_CONSUMERS 256
+// Consumer threads per CTA (one producer warp besides).  The plain kernel
+// folds with 4 consumer warps, the fused-blend kernel (twice the tiles per
+// stage, C blends per vector) with 8.  Alternating A/B builds on one GPU
+// (profiles/r02/ab_tma_consumers_n1.txt), BERT / ResNet-50 / GPT-2 config 4:
+// 128 consumers 0.995-0.997 / 0.965-0.969 / 0.764, 256: 0.948-0.951 /
+// 0.931-0.937 / 0.957-0.958, 384: 0.949-0.952 / 0.934-0.936 / 0.952-0.954,
+// 512: 0.948 / 0.929-0.931 / 0.940-0.945 of measured HBM.
+#ifndef RV_TMA_CONSUMERS  // A/B builds only override these
+#define RV_TMA_CONSUMERS 128
 #endif
-constexpr int kTmaConsumers = RV_TMA_CONSUMERS;
+#ifndef RV_TMA_BL_CONSUMERS
+#define RV_TMA_BL_CONSUMERS 256
+#endif
+__host__ __device__ constexpr int tma_consumers(bool bl) { return bl ? RV_TMA_BL_CONSUMERS : RV_TMA_CONSUMERS; }
 
 __device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -573,12 +584,13 @@ __host__ __device__ constexpr int tma_out_buffers(bool bl, int cb) {
 // live tile; the consumers write the mean tile and C blended live tiles,
 // which go out by bulk store to dst and live.
 template <typename T, typename Acc, int CB, int TV, int STAGES, bool BL = false>
-__global__ void __launch_bounds__(kTmaConsumers + 32, kTmaConsumers > 256 ? 1 : 2)
+__global__ void __launch_bounds__(tma_consumers(BL) + 32, tma_consumers(BL) > 256 ? 1 : 2)
 ring_tma_kernel(const __grid_constant__ CycleParams p) {
   constexpr int N = 16 / sizeof(T);
   constexpr int SLOTS = BL ? 2 * CB : CB;  // tiles per stage: src (ring order), then live
   constexpr int OUTS = BL ? CB + 1 : 1;    // output tiles: mean, then blended live
   constexpr int NOB = tma_out_buffers(BL, CB);  // output buffers (bulk-store groups in flight)
+  constexpr int NC = tma_consumers(BL);          // consumer threads
   extern __shared__ __align__(128) unsigned char smem[];
   uint4 *in = reinterpret_cast<uint4 *>(smem);                       // [STAGES][SLOTS][TV]
   uint4 *out = in + (size_t)STAGES * SLOTS * TV;                       // [NOB][OUTS][TV]
@@ -637,7 +649,7 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
     return;
   }
 
-  // consumers (256 threads)
+  // consumers (NC threads)
   const int c = tid - 32;
   int stage = 0;
   unsigned phase = 0;
@@ -650,8 +662,8 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
     const int cnt = (int)max((int64_t)0, min((int64_t)TV, nvec - j0));
     mbar_wait(&full[stage], phase);
     // consumer 0 finished the previous tile's store bookkeeping (out[ob] free)
-    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
-    for (int v = c; v < cnt; v += kTmaConsumers) {
+    asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
+    for (int v = c; v < cnt; v += NC) {
       Lanes<T, 16> x, o;
       Acc acc[N];
       x.raw = in[((size_t)stage * SLOTS + 0) * TV + v];
@@ -683,7 +695,7 @@ ring_tma_kernel(const __grid_constant__ CycleParams p) {
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
     if (c == 0) {
       mbar_arrive(&empty[stage]);  // every consumer has read this stage
       if (cnt > 0) {
