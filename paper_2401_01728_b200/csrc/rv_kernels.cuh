@@ -521,7 +521,8 @@ ring_ll_kernel(const __grid_constant__ CycleParams p) {
 // (profiles/r02/ab_tma_consumers_n1.txt), BERT / ResNet-50 / GPT-2 config 4:
 // 128 consumers 0.995-0.997 / 0.965-0.969 / 0.764, 256: 0.948-0.951 /
 // 0.931-0.937 / 0.957-0.958, 384: 0.949-0.952 / 0.934-0.936 / 0.952-0.954,
-// 512: 0.948 / 0.929-0.931 / 0.940-0.945 of measured HBM.
+// 512: 0.948 / 0.929-0.931 / 0.940-0.945 of measured HBM; for the blend
+// kernel 192 / 256 / 320 measured alike (ab_tma_bl_consumers_n1.txt).
 #ifndef RV_TMA_CONSUMERS  // A/B builds only override these
 #define RV_TMA_CONSUMERS 128
 #endif
